@@ -1,0 +1,174 @@
+/*
+ * selsync_b200.h -- C-ABI of the B200-native SelSync hot path.
+ *
+ * The reference (arXiv 2307.07950's desk-scale re-implementation,
+ * /root/reference/pkg/src/selsync) has no FFI: its hot path is Python/numpy
+ * behind the functions cited on each entry point below. This header is the
+ * boundary a binding (ctypes / cffi / pybind) attaches to; see INTEGRATION.md.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch / CUDA types in signatures
+ *     (streams travel as `void*` = cudaStream_t, 0 = legacy default stream);
+ *   - every function returns an int status: SS_OK or SS_ERR_*; the message of
+ *     the last failure on the calling thread is ss_last_error();
+ *   - "dev" arguments are device pointers (HBM), "host" arguments live in host
+ *     memory; device kernels are asynchronous on the given stream;
+ *   - a workspace (ss_workspace_bytes) is owned by one stream at a time.
+ *
+ * Build: nvcc -gencode arch=compute_100a,code=sm_100a (see __graft_entry__.py).
+ */
+#ifndef SELSYNC_B200_H
+#define SELSYNC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SS_API __attribute__((visibility("default")))
+#else
+#define SS_API
+#endif
+
+/* status codes; the Python shim maps them onto selsync's exception types
+   (errors.py:4-17): CONFIG -> ConfigError, SIGNAL -> SignalError */
+#define SS_OK 0
+#define SS_ERR_CONFIG 1
+#define SS_ERR_SIGNAL 2
+#define SS_ERR_CUDA 3
+
+/* bits of the per-rank int32 flag word written by the signal step. Word
+   values are 0/1 unless an error bit is set, so an allreduce-MAX over ranks
+   is the N-bit OR of wire.py:139-151 / runtime.py:319-333, and any rank's
+   error (>= 2) reaches every rank in the same collective. */
+#define SS_FLAG_SYNC 1    /* own vote: decide() == "sync" (signal.py:101-107) */
+#define SS_FLAG_ERR_NAN 2 /* observed NaN (signal.py:67-68); state unchanged */
+#define SS_FLAG_ERR_NEG 4 /* observed x < 0 (signal.py:69-70); state unchanged */
+
+/* GradSignalState (signal.py:41-61) as a 64-byte POD that lives in HBM for
+   the device path or in host memory for the scalar API. */
+typedef struct ss_signal_state {
+    double smoothing;      /* lambda in (0, 1] */
+    double ewma_current;
+    double ewma_previous;
+    double max_delta_seen;
+    double last_delta;     /* relative_change after the last observe; NaN if step_count < 2 */
+    double last_norm_sq;   /* last observed ||g||^2 */
+    int64_t step_count;
+    int32_t warmup;        /* >= 1; the "EWMA window" of the paper */
+    int32_t error;         /* sticky SS_FLAG_ERR_* bits of rejected observations */
+} ss_signal_state;
+
+/* one decision-trace row (MetricsRecord columns grad_norm_sq, ewma, delta_g,
+   decision; metrics.py:23-48), written into a device ring by the signal step */
+typedef struct ss_trace_row {
+    double grad_norm_sq;
+    double ewma;
+    double delta_g;        /* NaN where the reference records None (strategies.py:287) */
+    int32_t step;          /* 0-based observation index of this worker */
+    int32_t word;          /* SS_FLAG_* bits: own vote | errors */
+} ss_trace_row;
+
+SS_API int ss_abi_version(void);
+SS_API const char* ss_last_error(void);
+SS_API int ss_signal_state_size(void);
+SS_API int ss_trace_row_size(void);
+
+/* ---------------- host scalar API (no GPU needed) ---------------- */
+
+/* default_smoothing, signal.py:20-29 */
+SS_API int ss_default_smoothing(int32_t n_workers, double* out_host);
+/* DeltaThreshold validation, signal.py:32-38 */
+SS_API int ss_check_delta(double delta);
+/* GradSignalState(smoothing, warmup) + __post_init__, signal.py:41-61 */
+SS_API int ss_signal_init(ss_signal_state* st_host, double smoothing, int32_t warmup);
+/* observe, signal.py:64-83; st unchanged on error */
+SS_API int ss_signal_observe(ss_signal_state* st_host, double grad_norm_sq);
+/* relative_change, signal.py:86-98 */
+SS_API int ss_relative_change(const ss_signal_state* st_host, double* out_host);
+/* decide, signal.py:101-107: *sync_out = 1 for "sync", 0 for "local" */
+SS_API int ss_decide(const ss_signal_state* st_host, double delta, int32_t* sync_out_host);
+
+/* ---------------- device hot path (sm_100a) ---------------- */
+
+/* bytes of scratch (block partials + arrival counter) any kernel below needs;
+   the memory must be zeroed once (ss_workspace_reset) and is then self-resetting */
+SS_API int ss_workspace_bytes(int64_t* bytes_host);
+SS_API int ss_workspace_reset(void* ws_dev, void* stream);
+
+/* K1: ||g||^2 of one flat fp32 buffer in fp64, one launch, deterministic
+   two-pass finish (last-arriving block reduces the block partials in a fixed
+   order). Replaces float(grad @ grad), strategies.py:285. */
+SS_API int ss_norm_sq_f32(const float* g_dev, int64_t n, double* out_dev, void* ws_dev, void* stream);
+
+/* K1 over a list of tensors (pointer table, one logical launch per <= 256
+   tensors; the model's p.grad tensors need not be contiguous). ptrs/sizes are
+   HOST arrays of device pointers / element counts. out_dev and/or st_dev may
+   be NULL; with st_dev the signal step (K2) runs in the finishing block. */
+SS_API int ss_norm_sq_multi_f32(const float* const* ptrs_host, const int64_t* sizes_host, int32_t count,
+                         double* out_dev, ss_signal_state* st_dev, double delta,
+                         int32_t* word_dev, ss_trace_row* trace_dev, int32_t trace_cap,
+                         void* ws_dev, void* stream);
+
+/* K2 alone: observe + relative_change + decide on the device-resident state
+   for a device-resident ||g||^2 (_grad_and_signal strategies.py:283-288 +
+   decide :384). Writes the flag word and, if trace_dev != NULL, the row
+   trace_dev[step % trace_cap]. One thread. */
+SS_API int ss_signal_step(ss_signal_state* st_dev, const double* norm_sq_dev, double delta,
+                   int32_t* word_dev, ss_trace_row* trace_dev, int32_t trace_cap, void* stream);
+
+/* K1+K2 in one launch over a flat buffer (prescale / grads-aggregation order) */
+SS_API int ss_norm_signal_f32(const float* g_dev, int64_t n, ss_signal_state* st_dev, double delta,
+                       int32_t* word_dev, ss_trace_row* trace_dev, int32_t trace_cap,
+                       void* ws_dev, void* stream);
+
+/* K3: fused SGD (+momentum, +weight decay, optional Nesterov) in place:
+     d = g + wd*w; m = first ? d : mu*m + (1-dampening)*d; d = nesterov ? d + mu*m : m;
+     w = (w - lr*d) * s,  s = sync_scale if (sync_word_dev && *sync_word_dev & SS_FLAG_SYNC) else 1
+   With mu = wd = 0 this is sgd_step (model.py:215-221); s = 1/N pre-scales the
+   parameters for an allreduce-SUM (the 1/N of aggregate_mean, strategies.py:167).
+   m_dev may be NULL when momentum == 0. */
+SS_API int ss_sgd_update_f32(float* w_dev, const float* g_dev, float* m_dev, int64_t n, float lr,
+                      float momentum, float dampening, float weight_decay, int32_t nesterov,
+                      int32_t first_step, const int32_t* sync_word_dev, float sync_scale,
+                      void* stream);
+
+/* K13+K2: the fused parameter-aggregation step of _selsync_step
+   (strategies.py:378-384): one pass reads w, g, m and writes w, m while
+   accumulating ||g||^2; the finishing block runs the signal step and writes
+   the flag word. 20P bytes with momentum, 12P without. */
+SS_API int ss_update_norm_signal_f32(float* w_dev, const float* g_dev, float* m_dev, int64_t n, float lr,
+                              float momentum, float dampening, float weight_decay,
+                              int32_t nesterov, int32_t first_step, ss_signal_state* st_dev,
+                              double delta, int32_t* word_dev, ss_trace_row* trace_dev,
+                              int32_t trace_cap, void* ws_dev, void* stream);
+
+/* ---------------- simulated workers on one device ---------------- */
+
+/* aggregate_mean (strategies.py:159-168) over `count` replica buffers in
+   index order, result written back into every buffer (the PS broadcast of
+   runtime.py:285-287). bufs_host: HOST array of device pointers, count <= 64. */
+SS_API int ss_replica_average_f32(float* const* bufs_host, int32_t count, int64_t n, void* stream);
+
+/* the same reduction without the division: the allreduce-SUM that follows
+   a 1/N pre-scale in the update epilogue (ss_sgd_update_f32 sync_scale) */
+SS_API int ss_replica_sum_f32(float* const* bufs_host, int32_t count, int64_t n, void* stream);
+
+/* elementwise mean of `count` buffers into out_dev (may alias a source) */
+SS_API int ss_mean_f32(const float* const* bufs_host, int32_t count, int64_t n, float* out_dev,
+                void* stream);
+
+/* flag exchange of runtime.py:319-333 for replicas: max over the words,
+   written back to every word. words_host: HOST array of device pointers. */
+SS_API int ss_replica_flag_max_i32(int32_t* const* words_host, int32_t count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SELSYNC_B200_H */

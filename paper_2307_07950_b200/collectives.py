@@ -1,0 +1,91 @@
+"""Rank-group collectives of the SelSync step over torch.distributed.
+
+The reference relays everything through a parameter server (runtime.py:
+``_on_flags`` :319-333 for the flag OR, ``_close_round`` :275-294 for the
+parameter mean). Here there is no server: one process per GPU, NCCL over
+NVLink/NVSwitch, and two collectives per step --
+
+  C1  ``agree``:    allreduce(int32[1], MAX) of the flag word, every step
+  C2  ``average_``: allreduce(fp32[P], AVG) (or SUM after a 1/N pre-scale)
+
+Collectives are issued on the caller's current CUDA stream ordering (torch's
+ProcessGroupNCCL makes its NCCL stream wait on it and the current stream wait
+on the result; no host synchronisation). The same class runs over ``gloo`` on
+CPU tensors, which the world-size-2 CPU tests use.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from .errors import ConfigError, TransportError
+
+
+class RankGroup:
+    def __init__(self, group: Optional[dist.ProcessGroup] = None):
+        if not (dist.is_available() and dist.is_initialized()):
+            self.group = None
+            self.size = 1
+            self.rank = 0
+            self.backend = None
+            return
+        self.group = group
+        self.size = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.backend = str(dist.get_backend(group)).lower()
+
+    @property
+    def distributed(self) -> bool:
+        return self.size > 1
+
+    def _call(self, fn, *args, **kw):
+        try:
+            return fn(*args, group=self.group, **kw)
+        except RuntimeError as exc:  # NCCL / gloo failures surface as RuntimeError
+            raise TransportError(str(exc)) from exc
+
+    def agree(self, word: torch.Tensor) -> None:
+        """C1: every rank ends with the MAX of the words == OR of the votes."""
+        if word.dtype != torch.int32 or word.numel() != 1:
+            raise ConfigError("flag word must be a single int32")
+        if self.distributed:
+            self._call(dist.all_reduce, word, op=dist.ReduceOp.MAX)
+
+    def average_(self, buf: torch.Tensor) -> None:
+        """C2: in-place mean over ranks (aggregate_mean, strategies.py:159-168)."""
+        if not self.distributed:
+            return
+        if self.backend == "nccl":
+            self._call(dist.all_reduce, buf, op=dist.ReduceOp.AVG)
+        else:  # gloo has no AVG
+            self._call(dist.all_reduce, buf, op=dist.ReduceOp.SUM)
+            buf.div_(self.size)
+
+    def sum_(self, buf: torch.Tensor) -> None:
+        """C2 after the 1/N pre-scale fused into the update epilogue."""
+        if self.distributed:
+            self._call(dist.all_reduce, buf, op=dist.ReduceOp.SUM)
+
+    def broadcast_(self, buf: torch.Tensor, src_rank: int = 0) -> None:
+        """Bootstrap: replicas start identical (runtime.py:178-191)."""
+        if self.distributed:
+            src = dist.get_global_rank(self.group, src_rank) if self.group is not None else src_rank
+            self._call(dist.broadcast, buf, src=src)
+
+    def max_float(self, value: float, device) -> float:
+        """Max of a host scalar over ranks (bench timing: max over ranks)."""
+        if not self.distributed:
+            return float(value)
+        t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+        self._call(dist.all_reduce, t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self, device=None) -> None:
+        if self.distributed:
+            if self.backend == "nccl" and device is not None:
+                self._call(dist.barrier, device_ids=[torch.device(device).index])
+            else:
+                self._call(dist.barrier)

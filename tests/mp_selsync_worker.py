@@ -1,0 +1,58 @@
+"""torchrun worker for tests/test_multigpu.py: one rank per GPU, NCCL.
+
+Runs SelSyncStep on a golden case (its N must equal WORLD_SIZE) and saves the
+rank's decisions, trace rows and final parameters for the test to compare
+with the reference's golden trace."""
+
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+from conftest import _load_cases  # noqa: E402
+from oracle import selsync_oracle as O  # noqa: E402
+from paper_2307_07950_b200 import SelSyncConfig  # noqa: E402
+from paper_2307_07950_b200.step import SelSyncStep  # noqa: E402
+
+
+def main():
+    name, fuse, out = sys.argv[1], sys.argv[2] == "fused", Path(sys.argv[3])
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    c = _load_cases()[name]
+    assert c["n"] == world, (c["n"], world)
+    P = c["P"]
+    # rank 0 holds the init; everyone else starts from garbage and must be
+    # overwritten by the bootstrap broadcast (runtime.py:178-191)
+    init = torch.tensor(c["init"], dtype=torch.float32, device=dev) if rank == 0 else \
+        torch.full((P,), 7.0, device=dev)
+    g = torch.zeros(P, device=dev)
+    cfg = SelSyncConfig(delta=c["delta"], aggregation=c["aggregation"], warmup=c["warmup"],
+                        smoothing=c["smoothing"])
+    step = SelSyncStep(init, g, cfg, fuse=fuse)
+    for s in range(c["steps"]):
+        g.copy_(torch.from_numpy(O.synthetic_grad32(c["grad_seed"], rank, s, P)))
+        step.step(c["lr"])
+    torch.cuda.synchronize()
+    recs = step.records()
+    np.savez(out / f"{name}_{sys.argv[2]}_rank{rank}.npz",
+             decisions=np.array(step.decisions), ewma=np.array([r["ewma"] for r in recs]),
+             delta_g=np.array([np.nan if r["delta_g"] is None else r["delta_g"] for r in recs]),
+             params=init.double().cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,45 @@
+"""Real multi-GPU SelSync over NCCL (one process per GPU, torchrun) vs the
+reference's golden traces. Needs >= 2 GPUs on one box (gpurun --gpus 2/4);
+skipped otherwise -- the single-GPU suite covers N workers with ReplicaSelSync."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from test_parity_gpu import assert_trace_parity, params_close  # noqa: F401
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = Path(__file__).resolve().parents[1]
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def run_torchrun(n, name, mode, out):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29533",
+           str(ROOT / "tests" / "mp_selsync_worker.py"), name, mode, str(out)]
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                          env={**os.environ, "NCCL_DEBUG": "WARN"})
+    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("name,n", [("n2_lam0.5", 2), ("cfg0_n2_d0.3", 2), ("n4_mixed", 4),
+                                    ("n4_grads", 4), ("n8_mixed", 8)])
+@pytest.mark.parametrize("mode", ["fused", "prescale"])
+def test_nccl_ranks_match_reference(name, n, mode, tmp_path, golden_cases):
+    if NGPU < n:
+        pytest.skip(f"needs {n} GPUs")
+    run_torchrun(n, name, mode, tmp_path)
+    c = golden_cases[name]
+    for rank in range(n):
+        z = np.load(tmp_path / f"{name}_{mode}_rank{rank}.npz")
+        assert_trace_parity(z["decisions"], c["decision"][:, 0], c["delta_g"], c["delta"], c["warmup"])
+        np.testing.assert_allclose(z["ewma"], c["ewma"][:, rank], rtol=1e-5)
+        np.testing.assert_allclose(z["delta_g"], c["delta_g"][:, rank], rtol=1e-5, atol=1e-12)
+        params_close(z["params"], c["finals"][rank])

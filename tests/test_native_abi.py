@@ -1,0 +1,65 @@
+"""The C-ABI library loads on a CPU-only machine and exports exactly what
+include/selsync_b200.h declares; host entry points work without a GPU."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "selsync_b200.h").read_text()
+    return sorted(set(re.findall(r"SS_API\s+(?:const\s+)?\w+\*?\s+\**(ss_\w+)\s*\(", text)))
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for must in ("ss_norm_sq_f32", "ss_update_norm_signal_f32", "ss_signal_step",
+                 "ss_sgd_update_f32", "ss_signal_observe", "ss_decide"):
+        assert must in syms
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2307_07950_b200 import _native as N
+
+    lib = ctypes.CDLL(str(N.LIB_PATH))
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    # and the binding covers every declared symbol
+    assert sorted(N.EXPORTED) == declared_symbols()
+
+
+def test_struct_layouts():
+    from paper_2307_07950_b200 import _native as N
+
+    assert N.LIB.ss_signal_state_size() == ctypes.sizeof(N.SignalStateC) == 64
+    assert N.LIB.ss_trace_row_size() == ctypes.sizeof(N.TraceRowC) == 32
+    assert N.LIB.ss_abi_version() == 1
+    assert N.workspace_bytes() > 8 * 148
+
+
+def test_error_codes_map_to_reference_exceptions():
+    from paper_2307_07950_b200 import _native as N
+    from paper_2307_07950_b200.errors import ConfigError, SignalError
+
+    with pytest.raises(SignalError):
+        N.check(N.LIB.ss_check_delta(-1.0))
+    out = ctypes.c_double()
+    with pytest.raises(ConfigError):
+        N.check(N.LIB.ss_default_smoothing(0, ctypes.byref(out)))
+    # device entry points validate arguments before touching the GPU
+    with pytest.raises(ConfigError):
+        N.check(N.LIB.ss_norm_sq_f32(None, 10, None, None, None))
+    with pytest.raises(ConfigError):
+        N.check(N.LIB.ss_sgd_update_f32(None, None, None, -1, 0.1, 0, 0, 0, 0, 0, None, 1.0, None))
+
+
+def test_build_flags_target_sm100a():
+    from paper_2307_07950_b200 import _build
+
+    assert "arch=compute_100a,code=sm_100a" in _build.ARCH
+    assert "-lineinfo" in _build.FLAGS

@@ -1,0 +1,135 @@
+"""Decision-trace / EWMA / Delta / parameter parity of the B200 SelSync step
+with the CPU reference, on identical seeded fp32 gradients and parameters.
+
+Bar (BASELINE.json north_star): identical sync/local decision trace except
+steps where |Delta - delta| < 1e-6 relative; EWMA and Delta within 1e-5
+relative; parameters within 1e-5 relative in fp32 after all steps. Golden
+traces come from the UNMODIFIED reference (tests/golden/make_golden.py); the
+momentum / weight-decay cases (not in the reference) use the oracle's
+torch.optim.SGD restatement.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import case_names
+from oracle import selsync_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2307_07950_b200 import SelSyncConfig, SignalError  # noqa: E402
+from paper_2307_07950_b200.replicas import ReplicaSelSync  # noqa: E402
+from paper_2307_07950_b200.step import SelSyncStep  # noqa: E402
+
+DEV = torch.device("cuda:0")
+TIE_REL = 1e-6
+
+
+def assert_trace_parity(dec_got, dec_want, deltas_want, delta, warmup):
+    """Decisions identical except at ties |Delta - delta| < 1e-6 relative."""
+    for s, (a, b) in enumerate(zip(dec_got, dec_want)):
+        if a != b:
+            row = deltas_want[s]
+            tie = s >= warmup and any(
+                not math.isnan(d) and abs(d - delta) <= TIE_REL * max(abs(delta), 1e-300) for d in row)
+            assert tie, f"step {s}: got {'sync' if a else 'local'}, reference {'sync' if b else 'local'}"
+
+
+def params_close(got, want):
+    scale = np.abs(want).max()
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-5 * scale)
+
+
+def run_replicas(c, fuse, cfg=None, steps=None):
+    n, P, steps = c["n"], c["P"], steps or c["steps"]
+    cfg = cfg or SelSyncConfig(delta=c["delta"], aggregation=c["aggregation"], warmup=c["warmup"],
+                               smoothing=c["smoothing"])
+    rep = ReplicaSelSync(torch.tensor(c["init"], dtype=torch.float32, device=DEV), n, cfg, fuse=fuse)
+    for s in range(steps):
+        rep.set_grads([torch.from_numpy(O.synthetic_grad32(c["grad_seed"], w, s, P)).to(DEV)
+                       for w in range(n)])
+        rep.step(c["lr"])
+    torch.cuda.synchronize()
+    return rep
+
+
+@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "prescale"])
+@pytest.mark.parametrize("name", case_names())
+def test_replicas_match_reference_golden(name, fuse, golden_cases):
+    c = golden_cases[name]
+    rep = run_replicas(c, fuse)
+    steps, n = c["steps"], c["n"]
+    want_dec = c["decision"][:, 0]
+    assert_trace_parity(rep.decisions, want_dec, c["delta_g"], c["delta"], c["warmup"])
+    for w in range(n):
+        tr = rep.trace(w)[:steps]
+        np.testing.assert_allclose(tr["grad_norm_sq"], c["grad_norm_sq"][:, w], rtol=1e-12)
+        np.testing.assert_allclose(tr["ewma"], c["ewma"][:, w], rtol=1e-5)
+        np.testing.assert_allclose(tr["delta_g"], c["delta_g"][:, w], rtol=1e-5, atol=1e-12)
+        params_close(rep.params[w].double().cpu().numpy(), c["finals"][w])
+
+
+@pytest.mark.parametrize("mu,wd,nest,agg", [(0.9, 4e-4, False, "params"), (0.9, 4e-4, True, "params"),
+                                             (0.9, 0.0, False, "grads"), (0.0, 1e-3, False, "params")])
+@pytest.mark.parametrize("fuse", [True, False], ids=["fused", "prescale"])
+def test_replicas_momentum_match_oracle(mu, wd, nest, agg, fuse):
+    n, d, steps, seed, delta, warmup, lam, lr = 4, 250, 40, 3, 0.02, 5, None, 0.05
+    P = 2 * d + 2
+    init = O.init_params_linear(d, 5).astype(np.float32).astype(np.float64)
+    cfg = SelSyncConfig(delta=delta, aggregation=agg, warmup=warmup, smoothing=lam, momentum=mu,
+                        weight_decay=wd, nesterov=nest)
+    rep = ReplicaSelSync(torch.tensor(init, dtype=torch.float32, device=DEV), n, cfg, fuse=fuse)
+    for s in range(steps):
+        rep.set_grads([torch.from_numpy(O.synthetic_grad32(seed, w, s, P)).to(DEV) for w in range(n)])
+        rep.step(lr)
+    ref = O.simulate_selsync(init, n, steps, lambda w, s, _p: O.synthetic_grad32(seed, w, s, P),
+                             delta=delta, warmup=warmup, smoothing=lam, lr=lr, aggregation=agg,
+                             momentum=mu, weight_decay=wd, nesterov=nest)
+    assert 0 < ref.decision.sum() < steps
+    assert_trace_parity(rep.decisions, ref.decision, ref.delta_g, delta, warmup)
+    for w in range(n):
+        params_close(rep.params[w].double().cpu().numpy(), ref.finals[w])
+
+
+@pytest.mark.parametrize("agg,fuse", [("params", True), ("params", False), ("grads", True)])
+def test_single_rank_step_matches_oracle(agg, fuse):
+    """SelSyncStep (the per-rank NCCL path) at world size 1."""
+    d, steps, seed, delta, warmup, lr = 5000, 60, 11, 0.003, 4, 0.1
+    P = 2 * d + 2
+    init = O.init_params_linear(d, 2).astype(np.float32).astype(np.float64)
+    w = torch.tensor(init, dtype=torch.float32, device=DEV)
+    g = torch.zeros_like(w)
+    step = SelSyncStep(w, g, SelSyncConfig(delta=delta, aggregation=agg, warmup=warmup,
+                                           momentum=0.9, weight_decay=1e-4), fuse=fuse)
+    got = []
+    for s in range(steps):
+        g.copy_(torch.from_numpy(O.synthetic_grad32(seed, 0, s, P)))
+        got.append(step.step(lr) == "sync")
+    ref = O.simulate_selsync(init, 1, steps, lambda w_, s, _p: O.synthetic_grad32(seed, 0, s, P),
+                             delta=delta, warmup=warmup, lr=lr, aggregation=agg, momentum=0.9,
+                             weight_decay=1e-4)
+    assert 0 < ref.decision.sum() < steps
+    assert_trace_parity(got, ref.decision, ref.delta_g, delta, warmup)
+    recs = step.records()
+    np.testing.assert_allclose([r["ewma"] for r in recs], ref.ewma[:, 0], rtol=1e-12)
+    assert [r["decision"] == "sync" for r in recs] == got
+    params_close(w.double().cpu().numpy(), ref.finals[0])
+    st = step.signal_state()
+    assert st.step_count == steps and st.ewma_current == pytest.approx(ref.states[0].ewma_current, rel=1e-12)
+
+
+def test_nan_gradient_raises_signal_error():
+    w = torch.zeros(1000, device=DEV)
+    g = torch.ones_like(w)
+    step = SelSyncStep(w, g, SelSyncConfig(delta=0.1, warmup=1), fuse=False)
+    step.step(0.1)
+    g[3] = float("nan")
+    with pytest.raises(SignalError):
+        step.step(0.1)
+    assert step.signal_state().step_count == 1  # state unchanged (signal.py:67-68)
