@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""SelSync hot-path benchmark on B200 (contract: one JSON line from rank 0).
+
+Workload (BASELINE.json configs[4] at the north_star's target size): one
+SelSync step per iteration over a flattened fp32 model of P = 100M
+parameters, SGD with momentum 0.9 and weight decay 4e-4 (the paper's
+ResNet-101 optimizer), synthetic gradients already resident
+in HBM. A step is the whole hot path:
+
+  K13+K2 (fused update + ||g||^2 + EWMA/Delta/decide, one kernel)
+  -> C1 NCCL allreduce-MAX of the flag word
+  -> C2 NCCL allreduce-AVG of the 400 MB parameter buffer on sync steps.
+
+The headline ``value`` is steps/s of the whole job under a decision mix with
+exactly 50% sync steps (gradient ring with scales [1, 1, 1.5, 1.5], EWMA
+smoothing 1.0, delta 0.3: Delta alternates 0 / >= 0.55); the forced
+all-local (delta = 1e9) and all-sync (delta = 0) rates are measured in the
+same run under ``modes``. ``e2e`` is the same step through the public API
+with the gradient copied from pinned host memory every step and the
+decision row read back. ``cpu_baseline`` / ``--impl reference`` time the
+reference's float64 CPU path (oracle/cpu_path.py) on this host.
+
+Run: python bench.py [--gpus N --steps K --warmup W]; N > 1 under torchrun.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SelSync steps/s and hot-path GB/s vs HBM/NVLink roofline"
+FALLBACK_HBM_GBS = 6650.0
+NVLINK_NOMINAL_GBS = 900.0
+NVLINK_ALLREDUCE_MEASURED_GBS = 725.0  # B200_PROFILING.md: 8-rank all-reduce busbw at 1 GiB
+MIX_SCALES = [1.0, 1.0, 1.5, 1.5]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--P", type=int, default=100_000_000)
+    ap.add_argument("--momentum", type=float, default=0.9)
+    ap.add_argument("--weight-decay", type=float, default=4e-4)
+    ap.add_argument("--lr", type=float, default=0.1)
+    ap.add_argument("--no-fuse", action="store_true", help="pre-scale order (K1+K2, C1, K3*1/N, SUM)")
+    ap.add_argument("--collective", default="symm", choices=["symm", "nccl"],
+                    help="C2 back end at N > 1: device-conditional symmetric-memory kernel or host-branch NCCL")
+    ap.add_argument("--flag-exchange", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons while the GPU is busy."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.samples = []
+        self.ok = False
+        self.period = period_s
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as exc:  # no NVML: report it, never block the bench
+            self.err = str(exc)
+        self._stop = threading.Event()
+        self._t = None
+
+    def _reasons(self):
+        nv = self.nv
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        return int(fn(self.h))
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append((self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM),
+                                     self._reasons()))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._stop.clear()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t is not None:
+            self._stop.set()
+            self._t.join()
+            self._t = None
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": f"nvml unavailable: {self.err}"}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        mhz = sorted(s for s, _ in self.samples)
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        return {"sm_mhz": mhz[len(mhz) // 2], "sm_max_mhz": self.max_mhz,
+                "reasons": [n for b, n in self.REASONS.items() if bits & b], "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- CPU arm
+
+
+def cpu_run(n_workers, P, steps, warmup, args, budget_s):
+    """Time the reference's CPU path (oracle/cpu_path.py) on a bounded sample:
+    P_sample parameters per worker chosen so the run fits the budget, time
+    scaled linearly to P (every op on the path is a linear pass over P)."""
+    import numpy as np  # noqa: F401
+
+    from oracle.cpu_path import CpuSelSync
+
+    def make(p):
+        return CpuSelSync(n_workers, p, delta=0.3, warmup=1, smoothing=1.0, momentum=args.momentum,
+                          weight_decay=args.weight_decay, sync_pattern=MIX_SCALES, grad_ring=4)
+
+    probe_p = min(P, 2_000_000)
+    probe = make(probe_p)
+    probe.time_steps(2, args.lr)
+    t_probe = probe.time_steps(4, args.lr) / 4
+    probe.close()
+    per_elem = t_probe / probe_p
+    total_steps = steps + warmup
+    p_sample = int(min(P, max(8_000_000, budget_s / max(total_steps, 1) / max(per_elem, 1e-15))))
+    p_sample = min(p_sample, P)
+    cpu = make(p_sample)
+    cpu.time_steps(warmup, args.lr)
+    syncs0 = cpu.syncs
+    secs = cpu.time_steps(steps, args.lr)
+    syncs = cpu.syncs - syncs0
+    threads = cpu.threads
+    cpu.close()
+    per_step_full = secs / steps * (P / p_sample)
+    return {
+        "value": n_workers / per_step_full,
+        "unit": "steps/s",
+        "cores": threads,
+        "host_cpus": os.cpu_count(),
+        "kind": "port",
+        "sample": (f"{steps} timed steps of the reference's float64 SelSync step (oracle/cpu_path.py: "
+                   f"g@g, observe/decide, SGD+momentum+wd, flag OR, on sync f64 serialize + PS "
+                   f"np.stack().mean + deserialize) for {n_workers} worker(s) at P_sample={p_sample:,} "
+                   f"({syncs}/{steps} sync steps), scaled x{P / p_sample:.2f} to P={P:,}"),
+        "sec_per_step_sample": secs / steps,
+    }
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    budget = 150.0
+    base = cpu_run(world, args.P, args.steps, args.warmup, args, budget)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": base["value"],
+        "unit": "steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * world / base["value"],
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp64",
+        "data": "synthetic",
+        "config": workload_config(args, world),
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": base["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, world):
+    return {
+        "workload": (f"selsync hot-path step, flattened fp32 model P={args.P:,} (BASELINE configs[4] "
+                     f"microbench at the north_star 100M size), SGD momentum {args.momentum} wd "
+                     f"{args.weight_decay}, 50% sync decision mix"),
+        "P": args.P,
+        "n_workers": world,
+        "order": "prescale" if args.no_fuse else "fused",
+        "collective": args.collective if world > 1 else "none (single rank)",
+        "flag_exchange": args.flag_exchange if world > 1 else "none (single rank)",
+        "decision_mix": {"sync_frac": 0.5, "grad_scales": MIX_SCALES, "smoothing": 1.0, "delta": 0.3,
+                         "warmup": 1},
+        "parallelism": f"dp{world} (SelSync replicas, NCCL)",
+        "value_counts": "worker-steps: N ranks x K steps / (max-over-ranks device time)",
+        "l2": f"inputs exceed L2: w, g, m = {12 * args.P / 1e9:.2f} GB per step vs 126 MB L2",
+    }
+
+
+# ----------------------------------------------------------------- GPU arm
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2307_07950_b200 import SelSyncConfig
+    from paper_2307_07950_b200 import kernels as K
+    from paper_2307_07950_b200.collectives import RankGroup
+    from paper_2307_07950_b200.step import SelSyncStep
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    comm = RankGroup()
+    P = args.P
+    hbm_peak, hbm_src = peaks()
+
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    w = (torch.rand(P, generator=gen, device=dev) - 0.5) * 0.1
+    # gradient ring: steps k = 0..3 use scales [1, 1, 1.5, 1.5] -> ||g||^2 ratio 2.25
+    lo = torch.randn(P, generator=gen, device=dev) * MIX_SCALES[0]
+    hi = torch.randn(P, generator=gen, device=dev) * MIX_SCALES[2]
+    grads_ring = [lo, lo.clone(), hi, hi.clone()]
+    g = torch.empty(P, device=dev)
+    mom = torch.zeros(P, device=dev)
+
+    def make_step(delta, smoothing=1.0):
+        cfg = SelSyncConfig(delta=delta, warmup=1, smoothing=smoothing, momentum=args.momentum,
+                            weight_decay=args.weight_decay)
+        st = SelSyncStep(w, g, cfg, momentum_buffer=mom, group=comm, fuse=not args.no_fuse,
+                         collective=args.collective if world > 1 else None,
+                         flag_exchange=args.flag_exchange, trace_capacity=1 << 14, profile=True)
+        return st
+
+    def run(step, n, host_ring=None, host_row=None):
+        """n steps. Device-resident inputs: step_async (no host round-trip) when
+        the step branches on the device. host_ring: the public blocking API with
+        an H2D copy of the step's gradient from pinned host memory and a D2H of
+        the step's decision row inside every step."""
+        for _ in range(n):
+            k = step.steps_done % 4
+            if host_ring is not None:
+                g.copy_(host_ring[k], non_blocking=True)
+                step.step(args.lr)
+                host_row.copy_(step.signal.trace[:32], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+            else:
+                step.grads = grads_ring[k]  # bind this step's resident gradient
+                if step.async_capable:
+                    step.step_async(args.lr)
+                else:
+                    step.step(args.lr)
+
+    def timed(step, n, **kw):
+        comm.barrier(dev)
+        torch.cuda.synchronize()
+        launches0 = K.LAUNCHES
+        k0 = len(step.kernel_events)
+        s0 = len(step.sync_events)
+        d0 = step.steps_done
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        run(step, n, **kw)
+        b.record()
+        torch.cuda.synchronize()
+        step.synchronize()
+        comm.barrier(dev)
+        ms = comm.max_float(a.elapsed_time(b), dev)
+        kms = step.kernel_ms()[k0:]
+        sms = step.sync_ms()[s0:]
+        dec = step.decisions()[d0 - step.steps_done:]
+        return dict(ms=ms, decisions=dec, kernel_ms=kms, sync_ms=sms, launches=K.LAUNCHES - launches0)
+
+    clocks = ClockSampler(local)
+    # ---- headline: 50% sync mix, device-resident inputs
+    mixed = make_step(0.3)
+    run(mixed, args.warmup)
+    clocks.start()
+    res = timed(mixed, args.steps)
+    clocks.stop()
+    # ---- forced modes
+    modes = {}
+    for name, delta in (("all_local", 1e9), ("all_sync", 0.0)):
+        st = make_step(delta)
+        run(st, max(3, args.warmup))
+        modes[name] = timed(st, args.steps)
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_ring = [t.cpu().pin_memory() for t in grads_ring[:1] + grads_ring[2:3]]
+        host_ring = [host_ring[0], host_ring[0], host_ring[1], host_ring[1]]
+        row = torch.empty(32, dtype=torch.uint8, pin_memory=True)
+        st = make_step(0.3)
+        run(st, max(3, args.warmup), host_ring=host_ring, host_row=row)
+        e = timed(st, args.steps, host_ring=host_ring, host_row=row)
+        e2e = {"value": world * args.steps / (e["ms"] / 1e3), "unit": "steps/s",
+               "h2d_bytes_per_step": 4 * P * world, "d2h_bytes_per_step": 32 * world,
+               "ms_per_step": e["ms"] / args.steps,
+               "note": ("per step and rank: H2D of the fp32 gradient from pinned host memory, the "
+                        "SelSync step, D2H of the decision row (bytes summed over ranks)")}
+
+    ms_step = res["ms"] / args.steps
+    kms = sorted(res["kernel_ms"])
+    k_mean = sum(kms) / len(kms)
+    bytes_per_launch = (20 if args.momentum else 12) * P
+    if args.no_fuse:
+        bytes_per_launch = 4 * P
+    achieved = bytes_per_launch / (k_mean * 1e-3) / 1e9
+    sync_frac = sum(1 for d in res["decisions"] if d) / len(res["decisions"])
+    line = {
+        "metric": METRIC,
+        "value": world * 1e3 / ms_step,
+        "unit": "steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp32",
+        "data": "synthetic (seeded randn gradients resident in HBM; random-init flat parameters)",
+        "config": workload_config(args, world),
+        "observed_sync_frac": sync_frac,
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "ss_update_norm_signal_f32 (K13+K2: fused SGD-momentum-wd update + ||g||^2 + signal step)"
+            if not args.no_fuse else "ss_norm_signal_f32 (K1+K2)",
+            "achieved": achieved,
+            "peak": hbm_peak,
+            "peak_source": hbm_src,
+            "unit": "GB/s",
+            "frac": achieved / hbm_peak,
+            "traffic": traffic_from_profiles(P),
+            "algorithmic_bytes_per_launch": bytes_per_launch,
+            "kernel_ms_mean": k_mean,
+            "kernel_ms_median": kms[len(kms) // 2],
+            "kernel_share_of_step": k_mean / ms_step,
+        },
+        "gpu_launches": res["launches"],
+        "clocks": clocks.summary(),
+        "modes": {},
+    }
+    for name, m in modes.items():
+        ent = {"steps_per_s": world * args.steps / (m["ms"] / 1e3), "ms_per_step": m["ms"] / args.steps,
+               "kernel_ms_mean": sum(m["kernel_ms"]) / len(m["kernel_ms"])}
+        ent.update(exchange_stats(m, P, world))
+        line["modes"][name] = ent
+    line.update({"exchange": exchange_stats(res, P, world)} if world > 1 else {})
+    if e2e is not None:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_run(1, P, 3, 1, args, args.cpu_seconds)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def exchange_stats(m, P, world):
+    """C1+C2 timing per step kind. Symmetric path: one event pair per step
+    (local steps = flag agreement + early exit); NCCL path: pairs on sync
+    steps only. busbw = (4P / t) * 2(N-1)/N (nccl-tests convention)."""
+    if world < 2 or not m["sync_ms"]:
+        return {}
+    sms, dec = m["sync_ms"], m["decisions"]
+    if len(sms) == len(dec):
+        on_sync = [t for t, d in zip(sms, dec) if d]
+        on_local = [t for t, d in zip(sms, dec) if not d]
+    else:
+        on_sync, on_local = sms, []
+    out = {}
+    if on_local:
+        out["local_exchange_us_mean"] = 1e3 * sum(on_local) / len(on_local)
+    if on_sync:
+        t = sum(on_sync) / len(on_sync)
+        algbw = 4 * P / (t * 1e-3) / 1e9
+        busbw = algbw * 2 * (world - 1) / world
+        out["sync_exchange_ms_mean"] = t
+        out["nvlink"] = {"busbw": busbw, "algbw": algbw, "unit": "GB/s",
+                         "peak_nominal": NVLINK_NOMINAL_GBS, "frac_nominal": busbw / NVLINK_NOMINAL_GBS,
+                         "ref_nccl_allreduce_busbw_1GiB_8gpu": NVLINK_ALLREDUCE_MEASURED_GBS,
+                         "frac_of_ref": busbw / NVLINK_ALLREDUCE_MEASURED_GBS}
+    return out
+
+
+def traffic_from_profiles(P):
+    """dram read+write bytes per launch of the roofline kernel from the
+    committed ncu --set full summary for the same P, if one exists."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        ent = d.get(str(P))
+        return None if ent is None else ent["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -167,6 +167,38 @@ SS_API int ss_mean_f32(const float* const* bufs_host, int32_t count, int64_t n, 
    written back to every word. words_host: HOST array of device pointers. */
 SS_API int ss_replica_flag_max_i32(int32_t* const* words_host, int32_t count, void* stream);
 
+/* ---------------- device-side exchange over NVLink peer memory ---------------- */
+
+#define SS_SYMM_MAX_RANKS 16
+#define SS_SYMM_ERR_TIMEOUT 1
+
+/* bytes of each rank's signal region (flag slots + done slots, uint64 each) */
+SS_API int ss_symm_signal_bytes(int32_t world, int64_t* bytes_host);
+
+/* One launch per step, after the update kernel (and after the NCCL
+   allreduce-MAX of the flag word when exchange == 0):
+     exchange = 1: P2P flag exchange -- the N-bit OR of runtime.py:319-333 as a
+                   MAX over seq-tagged words posted into every peer's signal
+                   region; *word_dev: own word in, agreed word out;
+     exchange = 0: *word_dev already holds the agreed word (NCCL MAX).
+   If the agreed word is SS_FLAG_SYNC, the flat fp32 buffer is replaced on
+   every rank by the mean over ranks (runtime.py:275-294, strategies.py:159-168):
+   each rank reduces its 1/N shard (multimem.ld_reduce through the NVSwitch
+   when mc_dev != NULL, else P2P loads in rank order), applies `scale` (= 1/N)
+   in the epilogue and stores the result to every rank; an end barrier
+   precedes the kernel's exit. The decision never visits the host.
+     bufs_host[r] / pads_host[r]: rank r's buffer / signal region (peer-mapped
+     device addresses, HOST arrays); seq_dev: uint32 step counter (zero
+     initially, advanced by the kernel); ws_dev: a zeroed ss_workspace;
+     agreed_ring_dev (optional): agreed word per call, ring of ring_cap;
+     err_dev: set to SS_SYMM_ERR_TIMEOUT if a peer does not answer within
+     timeout_s (the kernel then exits instead of hanging). */
+SS_API int ss_symm_sync_f32(float* const* bufs_host, uint64_t* const* pads_host, float* mc_dev,
+                            int32_t rank, int32_t world, int64_t n, int32_t* word_dev,
+                            int32_t exchange, float scale, uint32_t* seq_dev, void* ws_dev,
+                            int32_t* agreed_ring_dev, int32_t ring_cap, int32_t* err_dev,
+                            double timeout_s, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

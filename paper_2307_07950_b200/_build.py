@@ -15,7 +15,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRC = PKG / "csrc" / "selsync_b200.cu"
+SRCS = [PKG / "csrc" / "selsync_b200.cu", PKG / "csrc" / "selsync_symm.cu"]
+DEPS = [*SRCS, PKG / "csrc" / "common.cuh"]
 HEADER = ROOT / "include" / "selsync_b200.h"
 OUT = PKG / "_lib" / "libselsync_b200.so"
 
@@ -44,7 +45,7 @@ def needs_build() -> bool:
     if not OUT.exists():
         return True
     mtime = OUT.stat().st_mtime
-    return any(p.stat().st_mtime > mtime for p in (SRC, HEADER))
+    return any(p.stat().st_mtime > mtime for p in (*DEPS, HEADER))
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -52,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
     tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *FLAGS, f"-I{HEADER.parent}", str(SRC), "-o", str(tmp)]
+    cmd = [nvcc(), *ARCH, *FLAGS, f"-I{HEADER.parent}", *map(str, SRCS), "-o", str(tmp)]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = proc.stdout + proc.stderr
     (OUT.parent / "build.log").write_text(" ".join(cmd) + "\n" + log)

@@ -96,6 +96,12 @@ _SIGS = {
     "ss_replica_sum_f32": ([POINTER(c_void_p), c_int32, c_int64, _P], c_int),
     "ss_mean_f32": ([POINTER(c_void_p), c_int32, c_int64, _P, _P], c_int),
     "ss_replica_flag_max_i32": ([POINTER(c_void_p), c_int32, _P], c_int),
+    "ss_symm_signal_bytes": ([c_int32, POINTER(c_int64)], c_int),
+    "ss_symm_sync_f32": (
+        [POINTER(c_void_p), POINTER(c_void_p), _P, c_int32, c_int32, c_int64, _P, c_int32, c_float,
+         _P, _P, _P, c_int32, _P, c_double, _P],
+        c_int,
+    ),
 }
 
 EXPORTED = tuple(_SIGS)

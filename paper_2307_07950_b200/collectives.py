@@ -89,3 +89,73 @@ class RankGroup:
                 self._call(dist.barrier, device_ids=[torch.device(device).index])
             else:
                 self._call(dist.barrier)
+
+
+SIGNAL_OFFSET = 8192  # our slots sit at the top of torch's 9216-byte signal pad
+
+
+class SymmetricParams:
+    """Flat fp32 buffer in symmetric (peer-mapped) memory + the device-side
+    SelSync exchange kernel ``ss_symm_sync_f32`` over it.
+
+    Allocation and address exchange use torch.distributed._symmetric_memory
+    (plumbing); the data path is our kernel: optional P2P flag exchange, then
+    -- only when the agreed flag word says sync -- the parameter mean written
+    into every rank's buffer (NVLS multimem when the switch supports it, P2P
+    loads/stores otherwise), with no host involvement.
+    """
+
+    def __init__(self, numel: int, device, comm: RankGroup, *, ring_capacity: int = 1 << 14,
+                 timeout_s: float = 30.0, use_multicast: bool = True):
+        import ctypes
+
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from . import _native as N
+
+        if comm.group is None and not comm.distributed:
+            raise ConfigError("symmetric memory needs an initialised process group")
+        self.device = torch.device(device)
+        self.comm = comm
+        group = comm.group if comm.group is not None else dist.group.WORLD
+        if hasattr(symm_mem, "enable_symm_mem_for_group"):
+            try:
+                symm_mem.enable_symm_mem_for_group(group.group_name)
+            except Exception:
+                pass
+        self.buf = symm_mem.empty(numel, dtype=torch.float32, device=self.device)
+        self.hdl = symm_mem.rendezvous(self.buf, group)
+        self.world = int(self.hdl.world_size)
+        self.rank = int(self.hdl.rank)
+        need = ctypes.c_int64(0)
+        N.check(N.LIB.ss_symm_signal_bytes(self.world, ctypes.byref(need)))
+        if SIGNAL_OFFSET + need.value > int(self.hdl.signal_pad_size):
+            raise ConfigError("signal pad too small for the exchange slots")
+        self.bufs = N.ptr_array([int(p) for p in self.hdl.buffer_ptrs])
+        self.pads = N.ptr_array([int(p) + SIGNAL_OFFSET for p in self.hdl.signal_pad_ptrs])
+        mc = int(self.hdl.multicast_ptr) if use_multicast else 0
+        self.multicast = bool(mc)
+        self.mc = mc or None
+        # our slots of the local pad start zeroed; everyone zeroes before anyone posts
+        pad = self.hdl.get_signal_pad(self.rank, [need.value // 8], torch.int64, SIGNAL_OFFSET // 8)
+        pad.zero_()
+        self.seq = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.ring_capacity = int(ring_capacity)
+        self.agreed = torch.zeros(self.ring_capacity, dtype=torch.int32, device=self.device)
+        self.timeout_s = float(timeout_s)
+        torch.cuda.synchronize(self.device)
+        comm.barrier(self.device)
+
+    def sync_(self, word: torch.Tensor, ws_ptr: int, *, exchange: bool, stream: int) -> None:
+        from . import _native as N
+
+        N.check(N.LIB.ss_symm_sync_f32(
+            self.bufs, self.pads, self.mc, self.rank, self.world, self.buf.numel(), word.data_ptr(),
+            int(exchange), 1.0 / self.world, self.seq.data_ptr(), ws_ptr, self.agreed.data_ptr(),
+            self.ring_capacity, self.err.data_ptr(), self.timeout_s, stream))
+
+    def check(self) -> None:
+        if int(self.err.item()) != 0:
+            raise TransportError("a peer did not answer the device-side exchange within "
+                                 f"{self.timeout_s:.0f} s")

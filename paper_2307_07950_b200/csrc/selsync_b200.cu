@@ -21,6 +21,7 @@
 // as the kernel retires.
 
 #include "selsync_b200.h"
+#include "common.cuh"
 
 #include <cuda_runtime.h>
 
@@ -532,6 +533,18 @@ int check_trace(ss_trace_row* trace, int32_t cap) {
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 }  // namespace
+
+namespace ss_internal {
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+int check_launch(const char* what) { return ::check_launch(what); }
+int sm_count() { return ::sm_count(); }
+}  // namespace ss_internal
 
 // =================================================================== C-ABI
 

@@ -1,43 +1,45 @@
 """``SelSyncStep`` -- one rank's selective-synchronization step on a B200.
 
 Mirrors ``_selsync_step`` (strategies.py:369-403) for the caller that used to
-be ``run_worker`` + the parameter server: a per-rank training loop that calls
-``step(lr)`` after ``loss.backward()`` has written the flat gradient buffer.
+be ``run_worker`` + the parameter server: a per-rank training loop calling
+``step(lr)`` after ``loss.backward()`` has filled the flat gradient buffer.
 
-Order of device work per step (parameter aggregation, the default):
+Device work per step, parameter aggregation (the default):
 
-  K13+K2  one kernel: local update w, m <- SGD(w, g, m) (the reference applies
-          it before the vote, :380-383) while reducing ||g||^2 in fp64; the
-          finishing block runs observe/relative_change/decide on the device
-          state and writes the int32 flag word          (:378-384, signal.py)
-  C1      NCCL allreduce-MAX of the flag word = OR of the N votes
-                                                        (runtime.py:319-333)
-  C2      on sync only: NCCL allreduce-AVG of the flat fp32 parameters
-                                                        (runtime.py:275-294)
+  K13+K2  one kernel: the local update w, m <- SGD(w, g, m) (the reference
+          applies it before the vote, :380-383) while reducing ||g||^2 in
+          fp64; the finishing block runs observe / relative_change / decide
+          on the device-resident state and writes the int32 flag word
+  C1      allreduce-MAX of the flag word = OR of the N votes (runtime.py:319-333)
+          -- NCCL (default) or the P2P exchange inside the C2 kernel
+  C2      sync steps only: the parameter mean (runtime.py:275-294)
 
-``fuse=False`` selects the pre-scale order instead: K1+K2, C1, then K3 whose
-epilogue multiplies the updated parameters by 1/N when the agreed word says
-sync, then allreduce-SUM. Its host read of the word overlaps K3.
+Two C2 back ends:
+  collective="symm" (default when world > 1): parameters live in symmetric
+      memory and ``ss_symm_sync_f32`` reads the agreed word ON THE DEVICE and
+      averages only when it says sync (NVLS multimem reduce + broadcast, 1/N
+      in the epilogue). No host round-trip: ``step_async`` enqueues a whole
+      step and returns immediately; the host reads decisions lazily.
+  collective="nccl": the host reads the agreed word (4-byte pinned copy) and
+      issues NCCL allreduce-AVG on sync steps. ``fuse=False`` selects the
+      pre-scale order instead: K1+K2, C1, K3 whose epilogue multiplies by 1/N
+      when the agreed word says sync (the host read overlaps K3), allreduce-SUM.
 
-Gradient aggregation (``aggregation="grads"``, :395-399): K1+K2, C1, then on
-sync allreduce-AVG of the gradients before the update, else the own gradient.
-
-The host learns the agreed decision through a 4-byte pinned copy of the word
-(an event wait); that is the only host<->device traffic of a step.
+Gradient aggregation (aggregation="grads", :395-399) uses the NCCL back end:
+K1+K2, C1, then on sync allreduce-AVG of the gradients, then the update.
 """
 
 from __future__ import annotations
 
-from typing import Optional
-
 import math
+from typing import Optional
 
 import torch
 
 from . import kernels as K
-from .collectives import RankGroup
+from .collectives import RankGroup, SymmetricParams
 from .config import SelSyncConfig
-from .errors import ConfigError, SignalError
+from .errors import ConfigError
 
 
 class SelSyncStep:
@@ -50,9 +52,12 @@ class SelSyncStep:
         momentum_buffer: Optional[torch.Tensor] = None,
         group=None,
         fuse: bool = True,
+        collective: Optional[str] = None,
+        flag_exchange: str = "nccl",
         trace_capacity: int = 4096,
         broadcast_init: bool = True,
         profile: bool = False,
+        timeout_s: float = 30.0,
     ):
         if not isinstance(config, SelSyncConfig):
             raise ConfigError("config must be a SelSyncConfig")
@@ -62,12 +67,24 @@ class SelSyncStep:
             raise ConfigError("params and grads must be flat fp32 vectors of the same length")
         self.config = config
         self.device = params.device
-        self.params = params
         self.grads = grads
         self.comm = group if isinstance(group, RankGroup) else RankGroup(group)
         self.world = self.comm.size
         self.worker_id = self.comm.rank
-        self.fuse = bool(fuse) and config.aggregation == "params"
+        if collective is None:
+            collective = "symm" if (self.world > 1 and config.aggregation == "params"
+                                    and self.comm.backend == "nccl") else "nccl"
+        if collective not in ("nccl", "symm"):
+            raise ConfigError(f"collective must be 'nccl' or 'symm', got {collective!r}")
+        if flag_exchange not in ("nccl", "p2p"):
+            raise ConfigError(f"flag_exchange must be 'nccl' or 'p2p', got {flag_exchange!r}")
+        if collective == "symm" and config.aggregation != "params":
+            raise ConfigError("the symmetric-memory exchange implements parameter aggregation")
+        if flag_exchange == "p2p" and collective != "symm":
+            raise ConfigError("the P2P flag exchange runs inside the symmetric-memory kernel")
+        self.collective = collective if self.world > 1 else "none"
+        self.flag_exchange = flag_exchange
+        self.fuse = (bool(fuse) or self.collective == "symm") and config.aggregation == "params"
         if config.momentum != 0.0:
             if momentum_buffer is None:
                 momentum_buffer = torch.zeros_like(params)
@@ -78,10 +95,17 @@ class SelSyncStep:
         self.smoothing = config.smoothing_for(self.world)
         self.signal = K.DeviceSignal(self.device, self.smoothing, config.warmup, trace_capacity)
         self.ws = K.Workspace(self.device)
+        self.symm = None
+        if self.collective == "symm":
+            self.symm = SymmetricParams(params.numel(), self.device, self.comm,
+                                        ring_capacity=trace_capacity, timeout_s=timeout_s)
+            self.symm.buf.copy_(params)
+            params = self.symm.buf  # the step owns the symmetric copy; use step.params
+        self.params = params
         self._word_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._ready = torch.cuda.Event()
         self.steps_done = 0
-        self.decisions: list[bool] = []
+        self._host_decisions: dict[int, bool] = {}
         self.lrs: list[float] = []
         self.profile = profile
         self.kernel_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
@@ -90,6 +114,11 @@ class SelSyncStep:
             self.comm.broadcast_(self.params, 0)
 
     # ------------------------------------------------------------------
+    @property
+    def async_capable(self) -> bool:
+        """True when a step never needs the host to learn the branch."""
+        return self.collective == "symm" or (self.collective == "none" and self.fuse)
+
     def _events(self, bucket):
         if not self.profile:
             return None
@@ -97,66 +126,147 @@ class SelSyncStep:
         bucket.append(pair)
         return pair
 
-    def _read_word(self, stream) -> int:
-        self._word_host.copy_(self.signal.word, non_blocking=True)
-        self._ready.record(stream)
-        return 0
+    def _hp(self, first: bool) -> dict:
+        c = self.config
+        return dict(momentum=c.momentum, dampening=c.dampening, weight_decay=c.weight_decay,
+                    nesterov=c.nesterov, first_step=first)
 
-    def step(self, lr: float) -> str:
-        """Run one SelSync step on the gradients currently in ``grads``.
-
-        Returns the agreed decision, ``"sync"`` or ``"local"``. Raises
-        SignalError on every rank if any rank observed a NaN norm."""
+    def _check_lr(self, lr) -> float:
         lr = float(lr)
         if not (lr >= 0.0) or not math.isfinite(lr):
             raise ConfigError(f"learning rate must be non-negative, got {lr}")
-        cfg = self.config
-        first = self.steps_done == 0
-        stream = torch.cuda.current_stream(self.device)
-        hp = dict(momentum=cfg.momentum, dampening=cfg.dampening, weight_decay=cfg.weight_decay,
-                  nesterov=cfg.nesterov, first_step=first)
-        ev = self._events(self.kernel_events)
-        if ev:
-            ev[0].record(stream)
-        if self.fuse:
-            K.update_norm_signal_(self.params, self.grads, self.momentum, self.signal, self.ws,
-                                  lr=lr, delta=cfg.delta, **hp)
-        else:
-            K.norm_signal(self.grads, self.signal, cfg.delta, self.ws)
-        if ev:
-            ev[1].record(stream)
-        self.comm.agree(self.signal.word)
-        self._read_word(stream)
-        if cfg.aggregation == "params" and not self.fuse:
-            # the host read above overlaps this update
-            K.sgd_update_(self.params, self.grads, self.momentum, lr=lr,
-                          sync_word=self.signal.word, sync_scale=1.0 / self.world, **hp)
+        return lr
+
+    def _wait_word(self, stream) -> int:
+        self._word_host.copy_(self.signal.word, non_blocking=True)
+        self._ready.record(stream)
         self._ready.synchronize()
         word = int(self._word_host[0])
         if word >= 2:
             K.raise_for_word(word, f" (agreed flag word {word} at step {self.steps_done})")
-        synced = bool(word & 1)
-        if cfg.aggregation == "params":
-            if synced and self.world > 1:
-                ev = self._events(self.sync_events)
-                if ev:
-                    ev[0].record(stream)
-                if self.fuse:
-                    self.comm.average_(self.params)
-                else:
-                    self.comm.sum_(self.params)
-                if ev:
-                    ev[1].record(stream)
-        else:
-            if synced and self.world > 1:
-                self.comm.average_(self.grads)
-            K.sgd_update_(self.params, self.grads, self.momentum, lr=lr, **hp)
+        return word
+
+    def _enqueue_device_step(self, lr: float, stream) -> None:
+        """K13+K2 -> C1 -> conditional C2, entirely on the device."""
+        cfg = self.config
+        ev = self._events(self.kernel_events)
+        if ev:
+            ev[0].record(stream)
+        K.update_norm_signal_(self.params, self.grads, self.momentum, self.signal, self.ws,
+                              lr=lr, delta=cfg.delta, **self._hp(self.steps_done == 0))
+        if ev:
+            ev[1].record(stream)
+        if self.collective == "symm":
+            ev = self._events(self.sync_events)
+            if ev:
+                ev[0].record(stream)
+            if self.flag_exchange == "nccl":
+                self.comm.agree(self.signal.word)
+            self.symm.sync_(self.signal.word, self.ws.ptr, exchange=self.flag_exchange == "p2p",
+                            stream=stream.cuda_stream)
+            K._count()
+            if ev:
+                ev[1].record(stream)
+
+    def step_async(self, lr: float) -> None:
+        """Enqueue one whole step and return without waiting for the GPU.
+        Needs a device-side branch (world size 1 or collective='symm')."""
+        if not self.async_capable:
+            raise ConfigError("step_async needs collective='symm' (or a single rank)")
+        lr = self._check_lr(lr)
+        self._enqueue_device_step(lr, torch.cuda.current_stream(self.device))
         self.steps_done += 1
-        self.decisions.append(synced)
+        self.lrs.append(lr)
+
+    def step(self, lr: float) -> str:
+        """Run one SelSync step on the gradients in ``grads``; returns the
+        agreed decision ``"sync"`` / ``"local"``. Raises SignalError on every
+        rank if any rank observed a NaN norm."""
+        lr = self._check_lr(lr)
+        cfg = self.config
+        stream = torch.cuda.current_stream(self.device)
+        if self.async_capable:
+            self._enqueue_device_step(lr, stream)
+            word = self._wait_word(stream)
+            if self.symm is not None:
+                self.symm.check()
+        else:
+            first = self.steps_done == 0
+            ev = self._events(self.kernel_events)
+            if ev:
+                ev[0].record(stream)
+            if self.fuse:
+                K.update_norm_signal_(self.params, self.grads, self.momentum, self.signal, self.ws,
+                                      lr=lr, delta=cfg.delta, **self._hp(first))
+            else:
+                K.norm_signal(self.grads, self.signal, cfg.delta, self.ws)
+            if ev:
+                ev[1].record(stream)
+            self.comm.agree(self.signal.word)
+            if cfg.aggregation == "params" and not self.fuse:
+                # the host read of the agreed word overlaps this update
+                self._word_host.copy_(self.signal.word, non_blocking=True)
+                self._ready.record(stream)
+                K.sgd_update_(self.params, self.grads, self.momentum, lr=lr,
+                              sync_word=self.signal.word, sync_scale=1.0 / self.world, **self._hp(first))
+                self._ready.synchronize()
+                word = int(self._word_host[0])
+                if word >= 2:
+                    K.raise_for_word(word, f" (agreed flag word {word} at step {self.steps_done})")
+            else:
+                word = self._wait_word(stream)
+            synced = bool(word & 1)
+            if cfg.aggregation == "params":
+                if synced and self.world > 1:
+                    ev = self._events(self.sync_events)
+                    if ev:
+                        ev[0].record(stream)
+                    if self.fuse:
+                        self.comm.average_(self.params)
+                    else:
+                        self.comm.sum_(self.params)
+                    if ev:
+                        ev[1].record(stream)
+            else:
+                if synced and self.world > 1:
+                    self.comm.average_(self.grads)
+                K.sgd_update_(self.params, self.grads, self.momentum, lr=lr, **self._hp(first))
+        synced = bool(word & 1)
+        self._host_decisions[self.steps_done] = synced
+        self.steps_done += 1
         self.lrs.append(lr)
         return "sync" if synced else "local"
 
     # ------------------------------------------------------------------
+    def synchronize(self) -> None:
+        """Wait for enqueued steps; raise on device-side errors (NaN norm, peer timeout)."""
+        torch.cuda.current_stream(self.device).synchronize()
+        if self.symm is not None:
+            self.symm.check()
+        s = self.signal.read_state()
+        if int(s["error"]):
+            K.raise_for_word(int(s["error"]) & 6 or 2, " (device signal state)")
+
+    def decisions(self) -> list[bool]:
+        """Agreed decision of every step still in the trace ring (True = sync)."""
+        cap = self.signal.trace_capacity
+        lo = max(0, self.steps_done - cap)
+        agreed = None
+        if self.symm is not None:
+            agreed = self.symm.agreed.cpu().numpy()
+        own = None
+        out = []
+        for s in range(lo, self.steps_done):
+            if s in self._host_decisions:
+                out.append(self._host_decisions[s])
+            elif agreed is not None:
+                out.append(bool(int(agreed[s % self.symm.ring_capacity]) == 1))
+            else:  # single rank: the agreed decision is the own vote
+                if own is None:
+                    own = self.signal.read_trace()
+                out.append(bool(int(own[s % cap]["word"]) & 1))
+        return out
+
     def signal_state(self):
         """Host copy of the device GradSignalState (signal.py:41-61)."""
         from .signal import GradSignalState
@@ -172,14 +282,16 @@ class SelSyncStep:
         steps still held by the device trace ring."""
         rows = self.signal.read_trace()
         cap = self.signal.trace_capacity
+        dec = self.decisions()
+        lo = max(0, self.steps_done - cap)
         out = []
-        for step in range(max(0, self.steps_done - cap), self.steps_done):
+        for i, step in enumerate(range(lo, self.steps_done)):
             r = rows[step % cap]
             d = float(r["delta_g"])
             out.append(dict(
                 step=step, worker_id=self.worker_id, grad_norm_sq=float(r["grad_norm_sq"]),
                 ewma=float(r["ewma"]), delta_g=None if math.isnan(d) else d,
-                decision="sync" if self.decisions[step] else "local",
+                decision="sync" if dec[i] else "local",
                 vote=bool(int(r["word"]) & 1), lr=self.lrs[step]))
         return out
 

@@ -24,7 +24,11 @@ from paper_2307_07950_b200.step import SelSyncStep  # noqa: E402
 
 
 def main():
-    name, fuse, out = sys.argv[1], sys.argv[2] == "fused", Path(sys.argv[3])
+    name, mode, out = sys.argv[1], sys.argv[2], Path(sys.argv[3])
+    opts = {"fused": dict(collective="nccl", fuse=True),
+            "prescale": dict(collective="nccl", fuse=False),
+            "symm-nccl": dict(collective="symm", flag_exchange="nccl"),
+            "symm-p2p": dict(collective="symm", flag_exchange="p2p")}[mode]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -40,16 +44,24 @@ def main():
     g = torch.zeros(P, device=dev)
     cfg = SelSyncConfig(delta=c["delta"], aggregation=c["aggregation"], warmup=c["warmup"],
                         smoothing=c["smoothing"])
-    step = SelSyncStep(init, g, cfg, fuse=fuse)
+    if c["aggregation"] != "params" and opts["collective"] == "symm":
+        opts = dict(collective="nccl", fuse=True)
+    step = SelSyncStep(init, g, cfg, **opts)
+    host = [torch.from_numpy(O.synthetic_grad32(c["grad_seed"], rank, s, P)).pin_memory()
+            for s in range(c["steps"])]
     for s in range(c["steps"]):
-        g.copy_(torch.from_numpy(O.synthetic_grad32(c["grad_seed"], rank, s, P)))
-        step.step(c["lr"])
-    torch.cuda.synchronize()
+        g.copy_(host[s], non_blocking=True)
+        if step.async_capable and s % 2:
+            step.step_async(c["lr"])  # device-side branch, no host round-trip
+        else:
+            step.step(c["lr"])
+    step.synchronize()
     recs = step.records()
-    np.savez(out / f"{name}_{sys.argv[2]}_rank{rank}.npz",
-             decisions=np.array(step.decisions), ewma=np.array([r["ewma"] for r in recs]),
+    np.savez(out / f"{name}_{mode}_rank{rank}.npz",
+             decisions=np.array(step.decisions()), ewma=np.array([r["ewma"] for r in recs]),
              delta_g=np.array([np.nan if r["delta_g"] is None else r["delta_g"] for r in recs]),
-             params=init.double().cpu().numpy())
+             params=step.params.double().cpu().numpy(),
+             multicast=np.array(bool(step.symm and step.symm.multicast)))
     dist.barrier()
     dist.destroy_process_group()
 

@@ -119,9 +119,34 @@ def test_single_rank_step_matches_oracle(agg, fuse):
     recs = step.records()
     np.testing.assert_allclose([r["ewma"] for r in recs], ref.ewma[:, 0], rtol=1e-12)
     assert [r["decision"] == "sync" for r in recs] == got
+    assert step.decisions() == got
     params_close(w.double().cpu().numpy(), ref.finals[0])
     st = step.signal_state()
     assert st.step_count == steps and st.ewma_current == pytest.approx(ref.states[0].ewma_current, rel=1e-12)
+
+
+def test_single_rank_async_steps_match_oracle():
+    """step_async: no host round-trip; decisions are read from the device ring afterwards."""
+    d, steps, seed, delta, warmup, lr = 3000, 80, 13, 0.003, 4, 0.1
+    P = 2 * d + 2
+    init = O.init_params_linear(d, 4).astype(np.float32).astype(np.float64)
+    w = torch.tensor(init, dtype=torch.float32, device=DEV)
+    g = torch.zeros_like(w)
+    step = SelSyncStep(w, g, SelSyncConfig(delta=delta, warmup=warmup, momentum=0.9, weight_decay=4e-4),
+                       trace_capacity=64)  # ring smaller than the run: wraps
+    assert step.async_capable
+    host = [torch.from_numpy(O.synthetic_grad32(seed, 0, s, P)).pin_memory() for s in range(steps)]
+    for s in range(steps):
+        g.copy_(host[s], non_blocking=True)
+        step.step_async(lr)
+    step.synchronize()
+    ref = O.simulate_selsync(init, 1, steps, lambda w_, s, _p: O.synthetic_grad32(seed, 0, s, P),
+                             delta=delta, warmup=warmup, lr=lr, momentum=0.9, weight_decay=4e-4)
+    assert 0 < ref.decision.sum() < steps
+    got = step.decisions()
+    assert len(got) == 64
+    assert_trace_parity(got, ref.decision[-64:], ref.delta_g[-64:], delta, -1)
+    params_close(w.double().cpu().numpy(), ref.finals[0])
 
 
 def test_nan_gradient_raises_signal_error():
