@@ -142,5 +142,14 @@ class FlatParameters:
     def zero_grad(self) -> None:
         self.grads.zero_()
 
+    def rebind(self, params: torch.Tensor) -> None:
+        """Point every ``p.data`` at views of another flat buffer with the same
+        layout (e.g. the symmetric-memory copy owned by a SelSyncStep)."""
+        if params.numel() != self.numel or params.dtype != torch.float32:
+            raise ConfigError("rebind needs a flat fp32 buffer of the same padded size")
+        for p, (off, shape) in zip(self.parameters, self.layout):
+            p.data = params[off: off + prod(shape)].view(shape)
+        self.params = params
+
     def vector(self) -> ParamVector:
         return ParamVector(self.params, self.layout)
