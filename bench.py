@@ -57,7 +57,8 @@ def parse():
     ap.add_argument("--no-fuse", action="store_true", help="pre-scale order (K1+K2, C1, K3*1/N, SUM)")
     ap.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                     help="C2 back end at N > 1: device-conditional symmetric-memory kernel or host-branch NCCL")
-    ap.add_argument("--flag-exchange", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--flag-exchange", default="fused", choices=["fused", "nccl", "p2p"],
+                    help="fused: the whole step in one cooperative launch (symm only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
@@ -271,7 +272,8 @@ def main():
                             weight_decay=args.weight_decay)
         st = SelSyncStep(w, g, cfg, momentum_buffer=mom, group=comm, fuse=not args.no_fuse,
                          collective=args.collective if world > 1 else None,
-                         flag_exchange=args.flag_exchange, trace_capacity=1 << 14, profile=True)
+                         flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
+                         trace_capacity=1 << 14, profile=True)
         return st
 
     def run(step, n, host_ring=None, host_row=None):
@@ -342,12 +344,20 @@ def main():
                         "SelSync step, D2H of the decision row (bytes summed over ranks)")}
 
     ms_step = res["ms"] / args.steps
-    kms = sorted(res["kernel_ms"])
+    one_launch = world > 1 and args.collective == "symm" and args.flag_exchange == "fused"
+    # roofline of the update kernel: its per-launch time on local steps (at
+    # N > 1 with the one-launch step this also holds the vote exchange)
+    kms = sorted(modes["all_local"]["kernel_ms"])
     k_mean = sum(kms) / len(kms)
     bytes_per_launch = (20 if args.momentum else 12) * P
     if args.no_fuse:
         bytes_per_launch = 4 * P
     achieved = bytes_per_launch / (k_mean * 1e-3) / 1e9
+    kernel_name = ("ss_update_norm_signal_f32 (K13+K2: fused SGD-momentum-wd update + ||g||^2 + signal step)"
+                   if not args.no_fuse else "ss_norm_signal_f32 (K1+K2)")
+    if one_launch:
+        kernel_name = ("ss_step_symm_f32 (one cooperative launch: K13+K2 + P2P vote exchange + "
+                       "conditional NVLink mean; timed on local steps)")
     sync_frac = sum(1 for d in res["decisions"] if d) / len(res["decisions"])
     line = {
         "metric": METRIC,
@@ -366,8 +376,7 @@ def main():
         "observed_sync_frac": sync_frac,
         "roofline": {
             "bound": "hbm",
-            "kernel": "ss_update_norm_signal_f32 (K13+K2: fused SGD-momentum-wd update + ||g||^2 + signal step)"
-            if not args.no_fuse else "ss_norm_signal_f32 (K1+K2)",
+            "kernel": kernel_name,
             "achieved": achieved,
             "peak": hbm_peak,
             "peak_source": hbm_src,
@@ -377,7 +386,8 @@ def main():
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "kernel_ms_mean": k_mean,
             "kernel_ms_median": kms[len(kms) // 2],
-            "kernel_share_of_step": k_mean / ms_step,
+            "kernel_share_of_local_step": k_mean / (modes["all_local"]["ms"] / args.steps),
+            "timed_on": "all_local mode, CUDA events around every launch on the launching stream",
         },
         "gpu_launches": res["launches"],
         "clocks": clocks.summary(),
@@ -389,6 +399,19 @@ def main():
         ent.update(exchange_stats(m, P, world))
         line["modes"][name] = ent
     line.update({"exchange": exchange_stats(res, P, world)} if world > 1 else {})
+    if one_launch:
+        # the mean runs inside the step launch: its cost is the sync-minus-local launch time
+        ks = modes["all_sync"]["kernel_ms"]
+        t = sum(ks) / len(ks) - k_mean
+        if t > 0:
+            algbw = 4 * P / (t * 1e-3) / 1e9
+            busbw = algbw * 2 * (world - 1) / world
+            line["exchange"] = {"sync_mean_ms_in_launch": t, "nvlink": {
+                "busbw": busbw, "algbw": algbw, "unit": "GB/s", "peak_nominal": NVLINK_NOMINAL_GBS,
+                "frac_nominal": busbw / NVLINK_NOMINAL_GBS,
+                "ref_nccl_allreduce_busbw_1GiB_8gpu": NVLINK_ALLREDUCE_MEASURED_GBS,
+                "frac_of_ref": busbw / NVLINK_ALLREDUCE_MEASURED_GBS,
+                "how": "(sync-step launch time - local-step launch time) of ss_step_symm_f32"}}
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

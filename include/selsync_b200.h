@@ -172,32 +172,54 @@ SS_API int ss_replica_flag_max_i32(int32_t* const* words_host, int32_t count, vo
 #define SS_SYMM_MAX_RANKS 16
 #define SS_SYMM_ERR_TIMEOUT 1
 
+/* A rank's view of the symmetric (peer-mapped) parameter buffer and of every
+   rank's signal region. Filled once by the host (e.g. from
+   torch.distributed._symmetric_memory.rendezvous); all pointers are device
+   addresses valid in this process. The signal regions hold 2*world uint64
+   slots (ss_symm_signal_bytes) and must start zeroed on every rank. */
+typedef struct ss_symm_group {
+    float* bufs[SS_SYMM_MAX_RANKS];     /* rank r's flat fp32 buffer */
+    uint64_t* pads[SS_SYMM_MAX_RANKS];  /* rank r's signal region */
+    float* mc;                          /* multicast (NVLS) address of the buffer, or NULL */
+    uint32_t* seq;                      /* step counter, zero-initialised, advanced by the kernels */
+    int32_t* agreed_ring;               /* optional ring of agreed words, one per step */
+    int32_t* err;                       /* set to SS_SYMM_ERR_TIMEOUT when a peer does not answer */
+    double timeout_s;                   /* bound of every spin (> 0) */
+    int32_t rank;
+    int32_t world;
+    int32_t ring_cap;
+    int32_t reserved;
+} ss_symm_group;
+
 /* bytes of each rank's signal region (flag slots + done slots, uint64 each) */
 SS_API int ss_symm_signal_bytes(int32_t world, int64_t* bytes_host);
 
-/* One launch per step, after the update kernel (and after the NCCL
-   allreduce-MAX of the flag word when exchange == 0):
+/* C2 (and optionally C1) as one launch after the update kernel:
      exchange = 1: P2P flag exchange -- the N-bit OR of runtime.py:319-333 as a
                    MAX over seq-tagged words posted into every peer's signal
                    region; *word_dev: own word in, agreed word out;
-     exchange = 0: *word_dev already holds the agreed word (NCCL MAX).
-   If the agreed word is SS_FLAG_SYNC, the flat fp32 buffer is replaced on
-   every rank by the mean over ranks (runtime.py:275-294, strategies.py:159-168):
-   each rank reduces its 1/N shard (multimem.ld_reduce through the NVSwitch
-   when mc_dev != NULL, else P2P loads in rank order), applies `scale` (= 1/N)
-   in the epilogue and stores the result to every rank; an end barrier
-   precedes the kernel's exit. The decision never visits the host.
-     bufs_host[r] / pads_host[r]: rank r's buffer / signal region (peer-mapped
-     device addresses, HOST arrays); seq_dev: uint32 step counter (zero
-     initially, advanced by the kernel); ws_dev: a zeroed ss_workspace;
-     agreed_ring_dev (optional): agreed word per call, ring of ring_cap;
-     err_dev: set to SS_SYMM_ERR_TIMEOUT if a peer does not answer within
-     timeout_s (the kernel then exits instead of hanging). */
-SS_API int ss_symm_sync_f32(float* const* bufs_host, uint64_t* const* pads_host, float* mc_dev,
-                            int32_t rank, int32_t world, int64_t n, int32_t* word_dev,
-                            int32_t exchange, float scale, uint32_t* seq_dev, void* ws_dev,
-                            int32_t* agreed_ring_dev, int32_t ring_cap, int32_t* err_dev,
-                            double timeout_s, void* stream);
+     exchange = 0: *word_dev already holds the agreed word (NCCL allreduce-MAX).
+   If the agreed word is SS_FLAG_SYNC, every rank's buffer is replaced by the
+   mean over ranks (runtime.py:275-294, strategies.py:159-168): each rank
+   reduces its 1/N shard (multimem.ld_reduce through the NVSwitch when
+   g->mc != NULL, else P2P loads in rank order), applies `scale` (= 1/N) in
+   the epilogue and stores the result to every rank; an end barrier precedes
+   the kernel's exit. The branch is taken on the device: no host round-trip.
+   g_host: HOST pointer to the group; ws_dev: a zeroed ss_workspace. */
+SS_API int ss_symm_sync_f32(const ss_symm_group* g_host, int64_t n, int32_t* word_dev,
+                            int32_t exchange, float scale, void* ws_dev, void* stream);
+
+/* The whole SelSync step in ONE cooperative launch (strategies.py:378-394):
+   fused update + ||g||^2 (K13) -> signal step in the finishing block (K2) ->
+   its vote posted to every peer -> every block waits for the N votes (C1) ->
+   on sync, the mean written into every rank's buffer with the 1/N applied in
+   the epilogue (C2) -> end barrier. w_dev must be g_host->bufs[g_host->rank].
+   *word_dev ends as the agreed word; the trace row keeps the own vote. */
+SS_API int ss_step_symm_f32(float* w_dev, const float* g_dev, float* m_dev, int64_t n, float lr,
+                            float momentum, float dampening, float weight_decay, int32_t nesterov,
+                            int32_t first_step, ss_signal_state* st_dev, double delta,
+                            int32_t* word_dev, ss_trace_row* trace_dev, int32_t trace_cap,
+                            const ss_symm_group* g_host, void* ws_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,27 @@ class TraceRowC(Structure):
     ]
 
 
+SYMM_MAX_RANKS = 16
+
+
+class SymmGroupC(Structure):
+    """ss_symm_group -- a rank's view of the symmetric buffer and signal slots."""
+
+    _fields_ = [
+        ("bufs", c_void_p * SYMM_MAX_RANKS),
+        ("pads", c_void_p * SYMM_MAX_RANKS),
+        ("mc", c_void_p),
+        ("seq", c_void_p),
+        ("agreed_ring", c_void_p),
+        ("err", c_void_p),
+        ("timeout_s", c_double),
+        ("rank", c_int32),
+        ("world", c_int32),
+        ("ring_cap", c_int32),
+        ("reserved", c_int32),
+    ]
+
+
 _P = c_void_p
 _SIGS = {
     "ss_abi_version": ([], c_int),
@@ -97,9 +118,10 @@ _SIGS = {
     "ss_mean_f32": ([POINTER(c_void_p), c_int32, c_int64, _P, _P], c_int),
     "ss_replica_flag_max_i32": ([POINTER(c_void_p), c_int32, _P], c_int),
     "ss_symm_signal_bytes": ([c_int32, POINTER(c_int64)], c_int),
-    "ss_symm_sync_f32": (
-        [POINTER(c_void_p), POINTER(c_void_p), _P, c_int32, c_int32, c_int64, _P, c_int32, c_float,
-         _P, _P, _P, c_int32, _P, c_double, _P],
+    "ss_symm_sync_f32": ([POINTER(SymmGroupC), c_int64, _P, c_int32, c_float, _P, _P], c_int),
+    "ss_step_symm_f32": (
+        [_P, _P, _P, c_int64, c_float, c_float, c_float, c_float, c_int32, c_int32,
+         _P, c_double, _P, _P, c_int32, POINTER(SymmGroupC), _P, _P],
         c_int,
     ),
 }

@@ -126,8 +126,8 @@ class SymmetricParams:
         N.check(N.LIB.ss_symm_signal_bytes(self.world, ctypes.byref(need)))
         if SIGNAL_OFFSET + need.value > int(self.hdl.signal_pad_size):
             raise ConfigError("signal pad too small for the exchange slots")
-        self.bufs = N.ptr_array([int(p) for p in self.hdl.buffer_ptrs])
-        self.pads = N.ptr_array([int(p) + SIGNAL_OFFSET for p in self.hdl.signal_pad_ptrs])
+        if self.world > N.SYMM_MAX_RANKS:
+            raise ConfigError(f"at most {N.SYMM_MAX_RANKS} ranks per symmetric group")
         # NVLS moves 4P(1 + 1/N) bytes per link direction, the P2P two-shot
         # 2(N-1)/N * 4P: multicast wins from N = 4 up (measured on B200:
         # N=2 P2P 603 us vs NVLS 1030 us; N=4 NVLS 897 us vs P2P 920 us at 400 MB)
@@ -144,16 +144,32 @@ class SymmetricParams:
         self.ring_capacity = int(ring_capacity)
         self.agreed = torch.zeros(self.ring_capacity, dtype=torch.int32, device=self.device)
         self.timeout_s = float(timeout_s)
+        g = N.SymmGroupC()
+        for r, p in enumerate(self.hdl.buffer_ptrs):
+            g.bufs[r] = int(p)
+        for r, p in enumerate(self.hdl.signal_pad_ptrs):
+            g.pads[r] = int(p) + SIGNAL_OFFSET
+        g.mc = self.mc
+        g.seq = self.seq.data_ptr()
+        g.agreed_ring = self.agreed.data_ptr()
+        g.err = self.err.data_ptr()
+        g.timeout_s = self.timeout_s
+        g.rank, g.world, g.ring_cap = self.rank, self.world, self.ring_capacity
+        self.group_c = g
+        self.group_ref = ctypes.byref(g)
         torch.cuda.synchronize(self.device)
         comm.barrier(self.device)
 
     def sync_(self, word: torch.Tensor, ws_ptr: int, *, exchange: bool, stream: int) -> None:
         from . import _native as N
 
-        N.check(N.LIB.ss_symm_sync_f32(
-            self.bufs, self.pads, self.mc, self.rank, self.world, self.buf.numel(), word.data_ptr(),
-            int(exchange), 1.0 / self.world, self.seq.data_ptr(), ws_ptr, self.agreed.data_ptr(),
-            self.ring_capacity, self.err.data_ptr(), self.timeout_s, stream))
+        N.check(N.LIB.ss_symm_sync_f32(self.group_ref, self.buf.numel(), word.data_ptr(), int(exchange),
+                                       1.0 / self.world, ws_ptr, stream))
+
+    @property
+    def one_launch_capable(self) -> bool:
+        """The fused one-launch step supports NVLS or P2P widths 2, 4, 8."""
+        return self.multicast or self.world in (2, 4, 8)
 
     def check(self) -> None:
         if int(self.err.item()) != 0:

@@ -22,6 +22,7 @@
 
 #include "selsync_b200.h"
 #include "common.cuh"
+#include "symm_device.cuh"
 
 #include <cuda_runtime.h>
 
@@ -305,8 +306,10 @@ __device__ __forceinline__ void sgd_elem(float& w, float g, float& m, const SgdA
     w = fmaf(-a.lr, d, w) * s;
 }
 
+// One streaming pass of the update over the whole buffer; returns this
+// thread's fp64 partial of ||g||^2 (0 when NORM is false).
 template <bool MOM, bool NEST, bool NORM, int U>
-__global__ void __launch_bounds__(kThreads) sgd_kernel(SgdArgs a, Finish f) {
+__device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     float s = 1.0f;
@@ -368,7 +371,83 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel(SgdArgs a, Finish f) {
         a.w[j] = w;
         if (MOM) a.m[j] = m;
     }
+    return acc;
+}
+
+template <bool MOM, bool NEST, bool NORM, int U>
+__global__ void __launch_bounds__(kThreads) sgd_kernel(SgdArgs a, Finish f) {
+    const double acc = sgd_pass<MOM, NEST, NORM, U>(a);
     if (NORM) finish_norm(f, acc);
+}
+
+// ------------------------------------------- the whole step in one launch
+//
+// K13 (update + ||g||^2) -> K2 in the last-arriving block -> its vote posted
+// to every peer's signal slot -> every block waits for the N votes (C1, MAX
+// = OR) -> on sync every block averages its part of this rank's shard over
+// NVLink with the 1/N in the epilogue (C2) -> end barrier in the last block.
+// Launched cooperatively: all blocks are co-resident, so blocks may wait for
+// the last one to publish the vote.
+template <bool MOM, bool NEST, int W>
+__global__ void __launch_bounds__(kThreads) step_kernel(SgdArgs a, Finish f, SymmArgs s) {
+    __shared__ bool s_last;
+    __shared__ int s_word;
+    __shared__ bool s_timeout;
+    const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
+    constexpr int U = MOM ? 2 : 4;
+    const double acc = sgd_pass<MOM, NEST, true, U>(a);
+    Workspace ws = ws_view(f.ws);
+    const double bsum = block_sum(acc);
+    if (threadIdx.x == 0) {
+        ws.partials[blockIdx.x] = bsum;
+        __threadfence_system();  // this block's parameter stores reach peers before the vote
+        s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        double v = 0.0;
+        for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
+        v = block_sum(v);
+        if (threadIdx.x == 0) {
+            *ws.counter = 0u;
+            signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+            const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+            __threadfence_system();
+            for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.rank, tagged);
+        }
+    }
+    if (threadIdx.x == 0) {
+        bool to = false;
+        int w = 0;
+        for (int j = 0; j < s.world && !to; ++j) {
+            const uint64_t v = wait_tag(s.pads[s.rank] + j, seq, 32, s, &to);
+            const int wj = static_cast<int>(static_cast<uint32_t>(v));
+            w = wj > w ? wj : w;
+        }
+        s_word = w;
+        s_timeout = to;
+        if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+    }
+    __syncthreads();
+    const bool sync = !s_timeout && s_word == SS_FLAG_SYNC;
+    if (sync) {
+        average_shard<W>(s);
+        __threadfence_system();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+        *f.word = s_timeout ? -1 : s_word;
+        if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = s_timeout ? -1 : s_word;
+        if (sync) {
+            for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.world + s.rank, seq);
+            bool to = false;
+            for (int j = 0; j < s.world && !to; ++j) wait_tag(s.pads[s.rank] + s.world + j, seq, 0, s, &to);
+            if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+        }
+        *s.arrive = 0u;
+        *s.seq = static_cast<uint32_t>(seq);
+    }
 }
 
 // ------------------------------------------------- multi-tensor K1 (+K2)
@@ -862,3 +941,65 @@ int ss_replica_flag_max_i32(int32_t* const* words, int32_t count, void* stream) 
 }
 
 }  // extern "C"
+
+namespace {
+
+template <bool MOM, bool NEST, int W>
+int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, void* stream) {
+    static int resident = 0;
+    if (resident == 0) {
+        int x = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, step_kernel<MOM, NEST, W>, kThreads, 0) != cudaSuccess || x <= 0)
+            x = 1;
+        resident = x;
+    }
+    constexpr int U = MOM ? 2 : 4;
+    const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, U, resident));
+    f.total_blocks = grid;
+    SgdArgs a2 = a;
+    SymmArgs s2 = sa;
+    void* args[] = {&a2, &f, &s2};
+    cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(step_kernel<MOM, NEST, W>), dim3(grid),
+                                                dim3(kThreads), args, 0, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(SS_ERR_CUDA, "ss_step_symm_f32: %s", cudaGetErrorString(e));
+    return check_launch("ss_step_symm_f32");
+}
+
+template <int W>
+int dispatch_step(const SgdArgs& a, const Finish& f, const SymmArgs& sa, bool mom, bool nest, void* stream) {
+    if (!mom) return launch_step<false, false, W>(a, f, sa, stream);
+    if (nest) return launch_step<true, true, W>(a, f, sa, stream);
+    return launch_step<true, false, W>(a, f, sa, stream);
+}
+
+}  // namespace
+
+extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, float lr, float momentum,
+                                float dampening, float weight_decay, int32_t nesterov, int32_t first_step,
+                                ss_signal_state* st, double delta, int32_t* word, ss_trace_row* trace,
+                                int32_t cap, const ss_symm_group* grp, void* ws, void* stream) {
+    SgdArgs a;
+    int rc = make_sgd_args(&a, w, g, m, n, lr, momentum, dampening, weight_decay, nesterov, first_step,
+                           nullptr, 1.0f);
+    if (rc) return rc;
+    if (!st || !ws || !word) return fail(SS_ERR_CONFIG, "null state/word/workspace");
+    rc = check_delta_impl(delta);
+    if (rc) return rc;
+    rc = check_trace(trace, cap);
+    if (rc) return rc;
+    SymmArgs sa;
+    rc = symm_args_from_group(grp, n, word, 1, 1.0f / static_cast<float>(grp ? grp->world : 1), ws, &sa,
+                              &ss_internal::fail);
+    if (rc) return rc;
+    if (grp->bufs[grp->rank] != w) return fail(SS_ERR_CONFIG, "w must be this rank's symmetric buffer");
+    Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
+    const bool mom = momentum != 0.0f, nest = nesterov != 0;
+    switch (symm_width(sa)) {
+        case 0: return dispatch_step<0>(a, f, sa, mom, nest, stream);
+        case 2: return dispatch_step<2>(a, f, sa, mom, nest, stream);
+        case 4: return dispatch_step<4>(a, f, sa, mom, nest, stream);
+        case 8: return dispatch_step<8>(a, f, sa, mom, nest, stream);
+        default:
+            return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 2, 4, 8)", sa.world);
+    }
+}

@@ -1,0 +1,232 @@
+// symm_device.cuh -- device helpers for the NVLink peer-memory exchange,
+// shared by the standalone exchange kernel (selsync_symm.cu) and the fused
+// one-launch step kernel (selsync_b200.cu). Internal; not part of the C-ABI.
+#pragma once
+
+#include "selsync_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace {
+
+constexpr int kMaxRanks = SS_SYMM_MAX_RANKS;
+struct SymmArgs {
+    float* bufs[kMaxRanks];      // peer buffer bases, index = rank
+    uint64_t* pads[kMaxRanks];   // peer signal regions: [0, W) flag slots, [W, 2W) done slots
+    float* mc;                   // multicast address of the buffer, nullptr -> P2P path
+    int rank, world;
+    int64_t n;
+    int32_t* word;               // exchange: own word in, agreed word out; else: agreed word
+    int exchange;
+    float scale;
+    uint32_t* seq;               // step counter (advanced by the last block)
+    unsigned int* arrive;        // block arrival counter (self-resetting)
+    int32_t* agreed_ring;        // optional: agreed word per step, ring of ring_cap
+    int32_t ring_cap;
+    int32_t* err;                // set to SS_SYMM_ERR_TIMEOUT on a timeout
+    uint64_t timeout_ns;
+};
+
+__device__ __forceinline__ uint64_t now_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ float4 mm_ld_reduce_add4(const float* p) {
+    float4 v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void mm_st4(float* p, float4 v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ float mm_ld_reduce_add1(const float* p) {
+    float v;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void mm_st1(float* p, float v) {
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
+// spin until (*p >> shift) == want (bounded); returns the last value read
+__device__ uint64_t wait_tag(const uint64_t* p, uint64_t want, int shift, const SymmArgs& a, bool* timed_out) {
+    const uint64_t t0 = now_ns();
+    uint64_t v = ld_acquire_sys(p);
+    while ((v >> shift) != want) {
+        if (now_ns() - t0 > a.timeout_ns) {
+            *timed_out = true;
+            return v;
+        }
+        __nanosleep(64);
+        v = ld_acquire_sys(p);
+    }
+    return v;
+}
+
+__device__ __forceinline__ float4 scale4(float4 v, float s) {
+    v.x *= s; v.y *= s; v.z *= s; v.w *= s;
+    return v;
+}
+
+// Shard of rank r: vectors [v0, v1) of the n/4 float4s; the scalar tail goes to the last rank.
+__device__ __forceinline__ void shard_range(const SymmArgs& a, int64_t* v0, int64_t* v1) {
+    const int64_t nvec = a.n >> 2;
+    const int64_t per = (nvec + a.world - 1) / a.world;
+    *v0 = per * a.rank < nvec ? per * a.rank : nvec;
+    *v1 = *v0 + per < nvec ? *v0 + per : nvec;
+}
+
+// NVLS: the switch reduces, multimem.st broadcasts (W = 0) -- or P2P two-shot
+// over W peers: all W loads of U vectors issued before any add (fixed rank
+// order => every rank's copy of a shard is bit-identical).
+template <int W>
+__device__ void average_shard(const SymmArgs& a) {
+    int64_t v0, v1;
+    shard_range(a, &v0, &v1);
+    const int64_t nvec = a.n >> 2;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int64_t i = v0 + tid;
+    if constexpr (W == 0) {
+        constexpr int U = 4;
+        for (; i + (U - 1) * stride < v1; i += U * stride) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = mm_ld_reduce_add4(a.mc + 4 * (i + u * stride));
+#pragma unroll
+            for (int u = 0; u < U; ++u) mm_st4(a.mc + 4 * (i + u * stride), scale4(v[u], a.scale));
+        }
+        for (; i < v1; i += stride) mm_st4(a.mc + 4 * i, scale4(mm_ld_reduce_add4(a.mc + 4 * i), a.scale));
+        if (a.rank == a.world - 1) {
+            for (int64_t j = 4 * nvec + tid; j < a.n; j += stride)
+                mm_st1(a.mc + j, mm_ld_reduce_add1(a.mc + j) * a.scale);
+        }
+    } else {
+        constexpr int U = W <= 2 ? 4 : (W <= 4 ? 2 : 1);
+        const float4* src[W];
+        float4* dst[W];
+#pragma unroll
+        for (int r = 0; r < W; ++r) {
+            src[r] = reinterpret_cast<const float4*>(a.bufs[r]);
+            dst[r] = reinterpret_cast<float4*>(a.bufs[r]);
+        }
+        for (; i + (U - 1) * stride < v1; i += U * stride) {
+            float4 v[U][W];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int r = 0; r < W; ++r) v[u][r] = __ldcg(src[r] + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float4 acc = v[u][0];
+#pragma unroll
+                for (int r = 1; r < W; ++r) {
+                    acc.x += v[u][r].x; acc.y += v[u][r].y; acc.z += v[u][r].z; acc.w += v[u][r].w;
+                }
+                acc = scale4(acc, a.scale);
+#pragma unroll
+                for (int r = 0; r < W; ++r) __stcg(dst[r] + i + u * stride, acc);
+            }
+        }
+        for (; i < v1; i += stride) {
+            float4 acc = __ldcg(src[0] + i);
+#pragma unroll
+            for (int r = 1; r < W; ++r) {
+                float4 v = __ldcg(src[r] + i);
+                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+            acc = scale4(acc, a.scale);
+#pragma unroll
+            for (int r = 0; r < W; ++r) __stcg(dst[r] + i, acc);
+        }
+        if (a.rank == a.world - 1) {
+            for (int64_t j = 4 * nvec + tid; j < a.n; j += stride) {
+                float acc = __ldcg(a.bufs[0] + j);
+#pragma unroll
+                for (int r = 1; r < W; ++r) acc += __ldcg(a.bufs[r] + j);
+                acc *= a.scale;
+#pragma unroll
+                for (int r = 0; r < W; ++r) __stcg(a.bufs[r] + j, acc);
+            }
+        }
+    }
+}
+
+
+}  // namespace
+
+namespace {
+
+// Validate a host ss_symm_group and build the kernel argument block.
+// ws: a zeroed ss_workspace; the exchange kernels use the arrival counter at
+// byte 64 (the norm reductions own the one at byte 0).
+inline int symm_args_from_group(const ss_symm_group* g, int64_t n, int32_t* word, int exchange,
+                                float scale, void* ws, SymmArgs* a, int (*fail_fn)(int, const char*, ...)) {
+    if (!g || !word || !ws) return fail_fn(SS_ERR_CONFIG, "null pointer argument");
+    if (g->world < 1 || g->world > kMaxRanks)
+        return fail_fn(SS_ERR_CONFIG, "world size must be in [1, %d], got %d", kMaxRanks, g->world);
+    if (g->rank < 0 || g->rank >= g->world)
+        return fail_fn(SS_ERR_CONFIG, "rank %d out of range for world %d", g->rank, g->world);
+    if (n < 0) return fail_fn(SS_ERR_CONFIG, "n must be >= 0");
+    if (!g->seq || !g->err) return fail_fn(SS_ERR_CONFIG, "null seq/err pointer in the group");
+    if (g->ring_cap < 0 || (g->agreed_ring && g->ring_cap == 0))
+        return fail_fn(SS_ERR_CONFIG, "bad agreed ring capacity");
+    if (!(g->timeout_s > 0.0)) return fail_fn(SS_ERR_CONFIG, "timeout must be positive");
+    for (int r = 0; r < kMaxRanks; ++r) {
+        a->bufs[r] = nullptr;
+        a->pads[r] = nullptr;
+    }
+    for (int r = 0; r < g->world; ++r) {
+        if (!g->bufs[r] || !g->pads[r]) return fail_fn(SS_ERR_CONFIG, "null peer pointer for rank %d", r);
+        if ((reinterpret_cast<uintptr_t>(g->bufs[r]) & 15) != 0)
+            return fail_fn(SS_ERR_CONFIG, "peer buffer %d not 16-byte aligned", r);
+        a->bufs[r] = g->bufs[r];
+        a->pads[r] = g->pads[r];
+    }
+    if (g->mc && (reinterpret_cast<uintptr_t>(g->mc) & 15) != 0)
+        return fail_fn(SS_ERR_CONFIG, "multicast address not 16-byte aligned");
+    a->mc = g->mc;
+    a->rank = g->rank;
+    a->world = g->world;
+    a->n = n;
+    a->word = word;
+    a->exchange = exchange ? 1 : 0;
+    a->scale = scale;
+    a->seq = g->seq;
+    a->arrive = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 64);
+    a->agreed_ring = g->agreed_ring;
+    a->ring_cap = g->ring_cap;
+    a->err = g->err;
+    a->timeout_ns = static_cast<uint64_t>(g->timeout_s * 1e9);
+    return SS_OK;
+}
+
+// P2P template width for a world size (0 = NVLS multicast path); -1 = unsupported
+inline int symm_width(const SymmArgs& a) {
+    if (a.mc) return 0;
+    return a.world <= 8 ? a.world : -1;
+}
+
+}  // namespace

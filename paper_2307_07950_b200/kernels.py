@@ -261,3 +261,20 @@ def raise_for_word(word: int, where: str = "") -> None:
 
 def isnan(x: float) -> bool:
     return isinstance(x, float) and math.isnan(x)
+
+
+def step_symm_(w, g, m, signal: DeviceSignal, ws: Workspace, group, *, lr: float, delta: float,
+               momentum: float = 0.0, dampening: float = 0.0, weight_decay: float = 0.0,
+               nesterov: bool = False, first_step: bool = False) -> None:
+    """The whole SelSync step in one cooperative launch (``ss_step_symm_f32``):
+    update + ||g||^2 + signal + P2P vote exchange + conditional NVLink mean.
+    ``group`` is a :class:`collectives.SymmetricParams`; ``w`` its buffer."""
+    _sgd_check(w, g, m, momentum)
+    if w.data_ptr() != group.buf.data_ptr():
+        raise ConfigError("w must be the symmetric parameter buffer")
+    N.check(N.LIB.ss_step_symm_f32(
+        w.data_ptr(), g.data_ptr(), _ptr(m) if momentum != 0.0 else None, w.numel(), float(lr),
+        float(momentum), float(dampening), float(weight_decay), int(bool(nesterov)),
+        int(bool(first_step)), signal.state.data_ptr(), float(delta), signal.word.data_ptr(),
+        signal.trace.data_ptr(), signal.trace_capacity, group.group_ref, ws.ptr, stream_of(w)))
+    _count()

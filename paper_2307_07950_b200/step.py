@@ -53,7 +53,7 @@ class SelSyncStep:
         group=None,
         fuse: bool = True,
         collective: Optional[str] = None,
-        flag_exchange: str = "nccl",
+        flag_exchange: Optional[str] = None,
         trace_capacity: int = 4096,
         broadcast_init: bool = True,
         profile: bool = False,
@@ -76,12 +76,14 @@ class SelSyncStep:
                                     and self.comm.backend == "nccl") else "nccl"
         if collective not in ("nccl", "symm"):
             raise ConfigError(f"collective must be 'nccl' or 'symm', got {collective!r}")
-        if flag_exchange not in ("nccl", "p2p"):
-            raise ConfigError(f"flag_exchange must be 'nccl' or 'p2p', got {flag_exchange!r}")
+        if flag_exchange is None:
+            flag_exchange = "fused" if collective == "symm" else "nccl"
+        if flag_exchange not in ("nccl", "p2p", "fused"):
+            raise ConfigError(f"flag_exchange must be 'fused', 'p2p' or 'nccl', got {flag_exchange!r}")
         if collective == "symm" and config.aggregation != "params":
             raise ConfigError("the symmetric-memory exchange implements parameter aggregation")
-        if flag_exchange == "p2p" and collective != "symm":
-            raise ConfigError("the P2P flag exchange runs inside the symmetric-memory kernel")
+        if flag_exchange in ("p2p", "fused") and collective != "symm":
+            raise ConfigError("the P2P flag exchange runs inside the symmetric-memory kernels")
         self.collective = collective if self.world > 1 else "none"
         self.flag_exchange = flag_exchange
         self.fuse = (bool(fuse) or self.collective == "symm") and config.aggregation == "params"
@@ -101,6 +103,8 @@ class SelSyncStep:
                                         ring_capacity=trace_capacity, timeout_s=timeout_s)
             self.symm.buf.copy_(params)
             params = self.symm.buf  # the step owns the symmetric copy; use step.params
+            if self.flag_exchange == "fused" and not self.symm.one_launch_capable:
+                self.flag_exchange = "p2p"
         self.params = params
         self._word_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._ready = torch.cuda.Event()
@@ -152,6 +156,13 @@ class SelSyncStep:
         ev = self._events(self.kernel_events)
         if ev:
             ev[0].record(stream)
+        if self.collective == "symm" and self.flag_exchange == "fused":
+            # one cooperative launch: update, norm, vote, vote exchange, conditional mean
+            K.step_symm_(self.params, self.grads, self.momentum, self.signal, self.ws, self.symm,
+                         lr=lr, delta=cfg.delta, **self._hp(self.steps_done == 0))
+            if ev:
+                ev[1].record(stream)
+            return
         K.update_norm_signal_(self.params, self.grads, self.momentum, self.signal, self.ws,
                               lr=lr, delta=cfg.delta, **self._hp(self.steps_done == 0))
         if ev:

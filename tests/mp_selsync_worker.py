@@ -28,7 +28,8 @@ def main():
     opts = {"fused": dict(collective="nccl", fuse=True),
             "prescale": dict(collective="nccl", fuse=False),
             "symm-nccl": dict(collective="symm", flag_exchange="nccl"),
-            "symm-p2p": dict(collective="symm", flag_exchange="p2p")}[mode]
+            "symm-p2p": dict(collective="symm", flag_exchange="p2p"),
+            "symm-fused": dict(collective="symm", flag_exchange="fused")}[mode]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
