@@ -51,13 +51,18 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--P", type=int, default=100_000_000)
+    ap.add_argument("--workload", default="microbench", choices=["microbench", "resnet101", "vgg11", "transformer"],
+                    help="microbench: the hot path on resident synthetic gradients (headline); model "
+                         "workloads add stock PyTorch fwd/bwd of BASELINE configs 1-3")
+    ap.add_argument("--delta", type=float, default=0.3, help="delta for model workloads")
+    ap.add_argument("--sel-warmup", type=int, default=25, help="EWMA window / warmup for model workloads")
     ap.add_argument("--momentum", type=float, default=0.9)
     ap.add_argument("--weight-decay", type=float, default=4e-4)
     ap.add_argument("--lr", type=float, default=0.1)
     ap.add_argument("--no-fuse", action="store_true", help="pre-scale order (K1+K2, C1, K3*1/N, SUM)")
     ap.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                     help="C2 back end at N > 1: device-conditional symmetric-memory kernel or host-branch NCCL")
-    ap.add_argument("--flag-exchange", default="fused", choices=["fused", "nccl", "p2p"],
+    ap.add_argument("--flag-exchange", default="p2p", choices=["p2p", "fused", "nccl"],
                     help="fused: the whole step in one cooperative launch (symm only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -257,6 +262,8 @@ def main():
     comm = RankGroup()
     P = args.P
     hbm_peak, hbm_src = peaks()
+    if args.workload != "microbench":
+        return model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src)
 
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     w = (torch.rand(P, generator=gen, device=dev) - 0.5) * 0.1
@@ -417,6 +424,94 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_run(1, P, 3, 1, args, args.cpu_seconds)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
+    """BASELINE configs 1-3: steps/s of fwd/bwd (stock PyTorch) + the SelSync hot path."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2307_07950_b200 import kernels as K
+    from paper_2307_07950_b200 import workloads as W
+    from paper_2307_07950_b200.train import SelSyncTrainer
+
+    wl = W.build(args.workload, dev, rank=rank, world=world)
+    P = W.parameter_count(wl.model)
+    tr = SelSyncTrainer(wl, delta=args.delta, warmup=args.sel_warmup, group=comm,
+                        collective=args.collective if world > 1 else None,
+                        flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
+                        trace_capacity=1 << 14, profile=True)
+    st = tr.step
+    for _ in range(args.warmup):
+        tr.train_step()
+    torch.cuda.synchronize()
+    comm.barrier(dev)
+    clocks = ClockSampler(local)
+    l0, k0, d0 = K.LAUNCHES, len(st.kernel_events), st.steps_done
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    a.record()
+    for _ in range(args.steps):
+        tr.train_step()
+    b.record()
+    torch.cuda.synchronize()
+    clocks.stop()
+    st.synchronize()
+    comm.barrier(dev)
+    ms = comm.max_float(a.elapsed_time(b), dev)
+    launches = K.LAUNCHES - l0
+    kms = st.kernel_ms()[k0:]
+    dec = st.decisions()[d0 - st.steps_done:]
+    k_mean = sum(kms) / len(kms)
+    nbytes = (20 if wl.momentum else 12) * st.params.numel()
+    # e2e: public blocking API, batch copied from pinned host memory, loss read back
+    e2e = None
+    if not args.no_e2e:
+        hb = [t.cpu().pin_memory() for t in wl.make_batch(0)]
+        db = [torch.empty_like(t, device=dev) for t in hb]
+        lh = torch.empty(1, pin_memory=True)
+        for i in range(args.warmup + args.steps):
+            if i == args.warmup:
+                torch.cuda.synchronize()
+                comm.barrier(dev)
+                ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ea.record()
+            for d_, h_ in zip(db, hb):
+                d_.copy_(h_, non_blocking=True)
+            loss, _ = tr.train_step(tuple(db), wait=True)
+            lh.copy_(loss.reshape(1), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        eb.record()
+        torch.cuda.synchronize()
+        ems = comm.max_float(ea.elapsed_time(eb), dev)
+        e2e = {"value": world * args.steps / (ems / 1e3), "unit": "steps/s",
+               "h2d_bytes_per_step": wl.host_batch_bytes * world, "d2h_bytes_per_step": 4 * world,
+               "ms_per_step": ems / args.steps}
+    line = {
+        "metric": METRIC, "value": world * args.steps / (ms / 1e3), "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic tensors of the config's shape, random-init weights",
+        "config": {"workload": f"{args.workload} (BASELINE configs): stock PyTorch fwd/bwd + SelSync hot path",
+                   "P": P, "P_padded": st.params.numel(), "delta": args.delta, "warmup": args.sel_warmup,
+                   "momentum": wl.momentum, "weight_decay": wl.weight_decay, "n_workers": world,
+                   "parallelism": f"dp{world} (SelSync replicas)",
+                   "value_counts": "worker-steps: N ranks x K steps / (max-over-ranks device time)"},
+        "observed_sync_frac": sum(dec) / max(1, len(dec)),
+        "roofline": {"bound": "hbm", "kernel": "SelSync update launch (K13+K2[+exchange])",
+                     "achieved": nbytes / (k_mean * 1e-3) / 1e9, "peak": hbm_peak, "peak_source": hbm_src,
+                     "unit": "GB/s", "frac": nbytes / (k_mean * 1e-3) / 1e9 / hbm_peak, "traffic": None,
+                     "kernel_ms_mean": k_mean, "hot_path_share_of_step": k_mean / (ms / args.steps)},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kThreads) sgd_kernel(SgdArgs a, Finish f) {
 // Launched cooperatively: all blocks are co-resident, so blocks may wait for
 // the last one to publish the vote.
 template <bool MOM, bool NEST, int W>
-__global__ void __launch_bounds__(kThreads) step_kernel(SgdArgs a, Finish f, SymmArgs s) {
+__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s) {
     __shared__ bool s_last;
     __shared__ int s_word;
     __shared__ bool s_timeout;

@@ -127,13 +127,25 @@ class FlatParameters:
         self.params = torch.zeros(self.numel, dtype=torch.float32, device=dev)
         self.grads = torch.zeros(self.numel, dtype=torch.float32, device=dev)
         self.momentum = torch.zeros(self.numel, dtype=torch.float32, device=dev) if momentum else None
+        # 4-D tensors already in channels_last keep that layout: their views into
+        # the flat buffers get NHWC strides (cuDNN then needs no weight transposes)
+        self.channels_last = [p.dim() == 4 and not p.is_contiguous()
+                              and p.is_contiguous(memory_format=torch.channels_last)
+                              for p in self.parameters]
         with torch.no_grad():
-            for p, (off, shape) in zip(self.parameters, self.layout):
-                n = prod(shape)
-                view = self.params[off: off + n].view(shape)
+            for p, (off, shape), cl in zip(self.parameters, self.layout, self.channels_last):
+                view = self._view(self.params, off, shape, cl)
                 view.copy_(p.data.to(device=dev, dtype=torch.float32))
                 p.data = view
-                p.grad = self.grads[off: off + n].view(shape)
+                p.grad = self._view(self.grads, off, shape, cl)
+
+    @staticmethod
+    def _view(buf: torch.Tensor, off: int, shape, channels_last: bool) -> torch.Tensor:
+        flat = buf[off: off + prod(shape)]
+        if channels_last:
+            n, c, h, w = shape
+            return flat.view(n, h, w, c).permute(0, 3, 1, 2)
+        return flat.view(shape)
 
     @property
     def n_real(self) -> int:
@@ -147,8 +159,8 @@ class FlatParameters:
         layout (e.g. the symmetric-memory copy owned by a SelSyncStep)."""
         if params.numel() != self.numel or params.dtype != torch.float32:
             raise ConfigError("rebind needs a flat fp32 buffer of the same padded size")
-        for p, (off, shape) in zip(self.parameters, self.layout):
-            p.data = params[off: off + prod(shape)].view(shape)
+        for p, (off, shape), cl in zip(self.parameters, self.layout, self.channels_last):
+            p.data = self._view(params, off, shape, cl)
         self.params = params
 
     def vector(self) -> ParamVector:

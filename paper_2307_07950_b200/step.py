@@ -77,7 +77,7 @@ class SelSyncStep:
         if collective not in ("nccl", "symm"):
             raise ConfigError(f"collective must be 'nccl' or 'symm', got {collective!r}")
         if flag_exchange is None:
-            flag_exchange = "fused" if collective == "symm" else "nccl"
+            flag_exchange = "p2p" if collective == "symm" else "nccl"
         if flag_exchange not in ("nccl", "p2p", "fused"):
             raise ConfigError(f"flag_exchange must be 'fused', 'p2p' or 'nccl', got {flag_exchange!r}")
         if collective == "symm" and config.aggregation != "params":
