@@ -82,7 +82,7 @@ class SelSyncStep:
             raise ConfigError(f"flag_exchange must be 'fused', 'p2p' or 'nccl', got {flag_exchange!r}")
         if collective == "symm" and config.aggregation != "params":
             raise ConfigError("the symmetric-memory exchange implements parameter aggregation")
-        if flag_exchange in ("p2p", "fused") and collective != "symm":
+        if flag_exchange in ("p2p", "fused") and collective != "symm" and self.world > 1:
             raise ConfigError("the P2P flag exchange runs inside the symmetric-memory kernels")
         self.collective = collective if self.world > 1 else "none"
         self.flag_exchange = flag_exchange

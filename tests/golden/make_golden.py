@@ -73,7 +73,7 @@ def synthetic_forward_backward(params, batch, spec):
     return 0.0, g
 
 
-def run_case(n, d, steps, delta, warmup, smoothing, lr, aggregation, init_seed):
+def run_case(n, d, steps, delta, warmup, smoothing, lr, aggregation, init_seed, name_for_metrics=None):
     ref_strategies.forward_backward = synthetic_forward_backward
     spec = ModelSpec(input_dim=d, hidden_dims=(), num_classes=2, init_seed=init_seed)
     strategy = SelSyncConfig(delta=delta, aggregation=aggregation, warmup=warmup, smoothing=smoothing)
@@ -89,6 +89,16 @@ def run_case(n, d, steps, delta, warmup, smoothing, lr, aggregation, init_seed):
         for w in range(n)
     ]
     res = run_simulation(ps, ctxs, cluster)
+    if name_for_metrics is not None:
+        from selsync.metrics import write_metrics_jsonl
+        from selsync.signal import replay_decisions
+
+        write_metrics_jsonl(res.rows, HERE / f"{name_for_metrics}_metrics.jsonl")
+        trace = [r.delta_g for r in sorted(res.rows, key=lambda r: r.step) if r.worker_id == 0]
+        grid = [0.0, 0.005, 0.01, 0.02, 0.05, 0.1, 1.0]
+        (HERE / f"{name_for_metrics}_replay.json").write_text(json.dumps(
+            {"worker": 0, "warmup": warmup, "grid": grid,
+             "syncs": [replay_decisions(trace, warmup, dd) for dd in grid]}))
     P = 2 * d + 2
     gn = np.zeros((steps, n))
     ew = np.zeros((steps, n))
@@ -152,7 +162,7 @@ def main():
     arrays = {}
     meta = {}
     for name, args in CASES.items():
-        res = run_case(*args)
+        res = run_case(*args, name_for_metrics=name if name == "n4_mixed" else None)
         n, d, steps, delta, warmup, smoothing, lr, agg, init_seed = args
         meta[name] = dict(n=n, d=d, P=2 * d + 2, steps=steps, delta=delta, warmup=warmup,
                           smoothing=smoothing, lr=lr, aggregation=agg, init_seed=init_seed,

@@ -158,3 +158,29 @@ def test_nan_gradient_raises_signal_error():
     with pytest.raises(SignalError):
         step.step(0.1)
     assert step.signal_state().step_count == 1  # state unchanged (signal.py:67-68)
+
+
+def test_device_trace_as_reference_metrics_jsonl(tmp_path, golden_cases):
+    """The B200 run's trace, written in the reference's metrics.jsonl schema,
+    replays to the same counterfactual sync counts as the reference's file."""
+    import json
+    from pathlib import Path
+
+    from paper_2307_07950_b200 import trace as T
+
+    c = golden_cases["n4_mixed"]
+    rep = run_replicas(c, True)
+    rows = T.to_metrics_rows(rep.records(), n_params=c["P"])
+    out = tmp_path / "metrics.jsonl"
+    T.write_metrics_jsonl(rows, out)
+    mine = T.load_metrics_jsonl(out)
+    gold_dir = Path(__file__).resolve().parent / "golden"
+    ref = T.load_metrics_jsonl(gold_dir / "n4_mixed_metrics.jsonl")
+    assert [(r["step"], r["worker_id"], r["decision"]) for r in mine] == \
+           [(r["step"], r["worker_id"], r["decision"]) for r in ref]
+    for a, b in zip(mine, ref):
+        assert a["ewma"] == pytest.approx(b["ewma"], rel=1e-12)
+        assert (a["delta_g"] is None) == (b["delta_g"] is None)
+    want = json.loads((gold_dir / "n4_mixed_replay.json").read_text())
+    got = T.replay_trace(mine, want["worker"], want["grid"], want["warmup"])
+    assert [n for _, n in got] == want["syncs"]
