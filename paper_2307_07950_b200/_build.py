@@ -31,7 +31,9 @@ FLAGS = [
     "-Xptxas",
     "-v",
     "--expt-relaxed-constexpr",
+    "-rdc=true",  # CUDA dynamic parallelism: the step kernel tail-launches the NVLink mean
 ]
+LIBS = ["-lcudadevrt"]
 
 
 def nvcc() -> str:
@@ -53,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return OUT
     OUT.parent.mkdir(parents=True, exist_ok=True)
     tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *FLAGS, f"-I{HEADER.parent}", *map(str, SRCS), "-o", str(tmp)]
+    cmd = [nvcc(), *ARCH, *FLAGS, f"-I{HEADER.parent}", *map(str, SRCS), *LIBS, "-o", str(tmp)]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = proc.stdout + proc.stderr
     (OUT.parent / "build.log").write_text(" ".join(cmd) + "\n" + log)

@@ -254,7 +254,7 @@ __device__ void finish_norm(const Finish& f, double acc) {
 // ---------------------------------------------------------------- K1
 
 template <int U>
-__global__ void __launch_bounds__(kThreads) norm_kernel(const float* __restrict__ g, int64_t n,
+__global__ void __launch_bounds__(kThreads, 4) norm_kernel(const float* __restrict__ g, int64_t n,
                                                         int64_t head, Finish f) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -375,25 +375,40 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
 }
 
 template <bool MOM, bool NEST, bool NORM, int U>
-__global__ void __launch_bounds__(kThreads) sgd_kernel(SgdArgs a, Finish f) {
+__global__ void __launch_bounds__(kThreads, 4) sgd_kernel(SgdArgs a, Finish f) {
     const double acc = sgd_pass<MOM, NEST, NORM, U>(a);
     if (NORM) finish_norm(f, acc);
 }
 
-// ------------------------------------------- the whole step in one launch
+// ------------------------------------------- the whole step in one host launch
 //
-// K13 (update + ||g||^2) -> K2 in the last-arriving block -> its vote posted
-// to every peer's signal slot -> every block waits for the N votes (C1, MAX
-// = OR) -> on sync every block averages its part of this rank's shard over
-// NVLink with the 1/N in the epilogue (C2) -> end barrier in the last block.
-// Launched cooperatively: all blocks are co-resident, so blocks may wait for
-// the last one to publish the vote.
+// step_kernel: K13 (update + ||g||^2) over the whole buffer; the last block
+// to arrive reduces the partials, runs K2, posts its vote to every peer's
+// signal slot and waits for the N votes (C1: MAX = OR). Every other block has
+// already exited, so a local step costs the update plus one NVLink round trip
+// in a single block. On sync the last block tail-launches avg_kernel (CUDA
+// dynamic parallelism, cudaStreamTailLaunch: it starts once this grid has
+// fully retired) which averages this rank's shard over NVLink with the 1/N in
+// the epilogue (C2) and closes with the end barrier. One host launch per step,
+// the branch never leaves the device.
+template <int W>
+__global__ void __launch_bounds__(512, 2) avg_kernel(SymmArgs s, uint64_t seq) {
+    average_shard<W>(s);
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+        for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.world + s.rank, seq);
+        bool to = false;
+        for (int j = 0; j < s.world && !to; ++j) wait_tag(s.pads[s.rank] + s.world + j, seq, 0, s, &to);
+        if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+        *s.arrive = 0u;
+        *s.seq = static_cast<uint32_t>(seq);
+    }
+}
+
 template <bool MOM, bool NEST, int W>
-__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s) {
+__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, int avg_grid) {
     __shared__ bool s_last;
-    __shared__ int s_word;
-    __shared__ bool s_timeout;
-    const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     constexpr int U = MOM ? 2 : 4;
     const double acc = sgd_pass<MOM, NEST, true, U>(a);
     Workspace ws = ws_view(f.ws);
@@ -404,48 +419,34 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
         s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (s_last) {
-        __threadfence();
-        double v = 0.0;
-        for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
-        v = block_sum(v);
-        if (threadIdx.x == 0) {
-            *ws.counter = 0u;
-            signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
-            const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
-            __threadfence_system();
-            for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.rank, tagged);
-        }
+    if (!s_last) return;
+    __threadfence();
+    double v = 0.0;
+    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
+    v = block_sum(v);
+    if (threadIdx.x != 0) return;
+    *ws.counter = 0u;
+    const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
+    signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+    const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+    __threadfence_system();
+    for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.rank, tagged);
+    bool to = false;
+    int w = 0;
+    for (int j = 0; j < s.world && !to; ++j) {
+        const uint64_t t = wait_tag(s.pads[s.rank] + j, seq, 32, s, &to);
+        const int wj = static_cast<int>(static_cast<uint32_t>(t));
+        w = wj > w ? wj : w;
     }
-    if (threadIdx.x == 0) {
-        bool to = false;
-        int w = 0;
-        for (int j = 0; j < s.world && !to; ++j) {
-            const uint64_t v = wait_tag(s.pads[s.rank] + j, seq, 32, s, &to);
-            const int wj = static_cast<int>(static_cast<uint32_t>(v));
-            w = wj > w ? wj : w;
-        }
-        s_word = w;
-        s_timeout = to;
-        if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+    if (to) {
+        atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+        w = -1;
     }
-    __syncthreads();
-    const bool sync = !s_timeout && s_word == SS_FLAG_SYNC;
-    if (sync) {
-        average_shard<W>(s);
-        __threadfence_system();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
-        *f.word = s_timeout ? -1 : s_word;
-        if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = s_timeout ? -1 : s_word;
-        if (sync) {
-            for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.world + s.rank, seq);
-            bool to = false;
-            for (int j = 0; j < s.world && !to; ++j) wait_tag(s.pads[s.rank] + s.world + j, seq, 0, s, &to);
-            if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
-        }
-        *s.arrive = 0u;
+    *f.word = w;
+    if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
+    if (w == SS_FLAG_SYNC) {
+        avg_kernel<W><<<avg_grid, 512, 0, cudaStreamTailLaunch>>>(s, seq);
+    } else {
         *s.seq = static_cast<uint32_t>(seq);
     }
 }
@@ -509,7 +510,7 @@ struct PtrTable {
 };
 
 template <bool VEC, bool BCAST>
-__global__ void __launch_bounds__(kThreads) mean_kernel(PtrTable t, int count, int64_t n, float* out,
+__global__ void __launch_bounds__(kThreads, 4) mean_kernel(PtrTable t, int count, int64_t n, float* out,
                                                         bool divide) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -946,22 +947,25 @@ namespace {
 
 template <bool MOM, bool NEST, int W>
 int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, void* stream) {
-    static int resident = 0;
+    static int resident = 0, avg_resident = 0;
     if (resident == 0) {
         int x = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, step_kernel<MOM, NEST, W>, kThreads, 0) != cudaSuccess || x <= 0)
             x = 1;
         resident = x;
+        x = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, avg_kernel<W>, 512, 0) != cudaSuccess || x <= 0) x = 1;
+        avg_resident = x;
     }
     constexpr int U = MOM ? 2 : 4;
     const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, U, resident));
     f.total_blocks = grid;
-    SgdArgs a2 = a;
-    SymmArgs s2 = sa;
-    void* args[] = {&a2, &f, &s2};
-    cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(step_kernel<MOM, NEST, W>), dim3(grid),
-                                                dim3(kThreads), args, 0, static_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) return fail(SS_ERR_CUDA, "ss_step_symm_f32: %s", cudaGetErrorString(e));
+    // averaging grid: every block co-resident (the last one runs the end barrier)
+    int avg_grid = sm_count() * avg_resident;
+    const int64_t per_rank_vec = ((sa.n >> 2) + sa.world - 1) / sa.world;
+    const int64_t want = (per_rank_vec + 512 * 4 - 1) / (512 * 4);
+    if (want < avg_grid) avg_grid = static_cast<int>(want < 1 ? 1 : want);
+    step_kernel<MOM, NEST, W><<<grid, kThreads, 0, as_stream(stream)>>>(a, f, sa, avg_grid);
     return check_launch("ss_step_symm_f32");
 }
 

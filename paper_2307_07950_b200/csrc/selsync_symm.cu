@@ -40,7 +40,7 @@ namespace {
 constexpr int kThreads = 512;
 
 template <int W>
-__global__ void __launch_bounds__(kThreads) symm_sync_kernel(SymmArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     __shared__ int s_word;
     __shared__ bool s_timeout;
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(a.seq)) + 1;
