@@ -30,6 +30,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -60,6 +61,7 @@ constexpr int kMaxGrid = 8192;
 constexpr int64_t kWsHeader = 256;  // arrival counter, padded to its own sector group
 constexpr int kMtMax = 256;         // tensors per multi-tensor launch (kernel-param table)
 constexpr int kMaxReplicas = 64;
+constexpr int kNormUnroll = 4;
 
 struct Workspace {
     unsigned int* counter;
@@ -181,6 +183,43 @@ __device__ void signal_step_dev(ss_signal_state* st, double x, double delta, int
 }
 
 // ----------------------------------------------------- memory helpers
+
+// cache policies for the streaming update (selected per instantiation; 0 is the default):
+//   0: ld/st .cs (evict-first)     1: plain ld/st
+//   2: ld .L1::no_allocate.L2::256B prefetch, st .cs
+//   3: like 2, gradient through the non-coherent path (ld.global.nc)
+template <int CP>
+__device__ __forceinline__ float4 ld_pol(const float* p) {
+    if constexpr (CP == 1) {
+        return *reinterpret_cast<const float4*>(p);
+    } else if constexpr (CP >= 2) {
+        float4 v;
+        asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+        return v;
+    } else {
+        return __ldcs(reinterpret_cast<const float4*>(p));
+    }
+}
+template <int CP>
+__device__ __forceinline__ float4 ld_pol_ro(const float* p) {
+    if constexpr (CP == 3) {
+        float4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+        return v;
+    } else {
+        return ld_pol<CP>(p);
+    }
+}
+template <int CP>
+__device__ __forceinline__ void st_pol(float* p, float4 v) {
+    if constexpr (CP == 1) {
+        *reinterpret_cast<float4*>(p) = v;
+    } else {
+        __stcs(reinterpret_cast<float4*>(p), v);
+    }
+}
 
 __device__ __forceinline__ float4 ld_cs4(const float* p) {
     return __ldcs(reinterpret_cast<const float4*>(p));
@@ -308,7 +347,7 @@ __device__ __forceinline__ void sgd_elem(float& w, float g, float& m, const SgdA
 
 // One streaming pass of the update over the whole buffer; returns this
 // thread's fp64 partial of ||g||^2 (0 when NORM is false).
-template <bool MOM, bool NEST, bool NORM, int U>
+template <bool MOM, bool NEST, bool NORM, int U, int CP = 0>
 __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -334,9 +373,9 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t k = 4 * (i + u * stride);
-            gv[u] = ld_cs4(gb + k);
-            wv[u] = ld_cs4(wb + k);
-            if (MOM) mv[u] = ld_cs4(mb + k);
+            gv[u] = ld_pol_ro<CP>(gb + k);
+            wv[u] = ld_pol<CP>(wb + k);
+            if (MOM) mv[u] = ld_pol<CP>(mb + k);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -347,8 +386,8 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
             sgd_elem<MOM, NEST>(wv[u].y, gv[u].y, mm.y, a, s);
             sgd_elem<MOM, NEST>(wv[u].z, gv[u].z, mm.z, a, s);
             sgd_elem<MOM, NEST>(wv[u].w, gv[u].w, mm.w, a, s);
-            st_cs4(wb + k, wv[u]);
-            if (MOM) st_cs4(mb + k, mm);
+            st_pol<CP>(wb + k, wv[u]);
+            if (MOM) st_pol<CP>(mb + k, mm);
         }
     }
     for (; i < nvec; i += stride) {
@@ -374,9 +413,9 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
     return acc;
 }
 
-template <bool MOM, bool NEST, bool NORM, int U>
+template <bool MOM, bool NEST, bool NORM, int U, int CP = 0>
 __global__ void __launch_bounds__(kThreads, 4) sgd_kernel(SgdArgs a, Finish f) {
-    const double acc = sgd_pass<MOM, NEST, NORM, U>(a);
+    const double acc = sgd_pass<MOM, NEST, NORM, U, CP>(a);
     if (NORM) finish_norm(f, acc);
 }
 
@@ -409,8 +448,7 @@ __global__ void __launch_bounds__(512, 2) avg_kernel(SymmArgs s, uint64_t seq) {
 template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, int avg_grid) {
     __shared__ bool s_last;
-    constexpr int U = MOM ? 2 : 4;
-    const double acc = sgd_pass<MOM, NEST, true, U>(a);
+    const double acc = sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
     Workspace ws = ws_view(f.ws);
     const double bsum = block_sum(acc);
     if (threadIdx.x == 0) {
@@ -612,6 +650,32 @@ int check_trace(ss_trace_row* trace, int32_t cap) {
 
 inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+template <int U>
+int launch_norm_u(const float* g, int64_t n, Finish f, void* stream, const char* what) {
+    static const int resident = resident_blocks(norm_kernel<U>);
+    const int64_t head = n ? common_head(n, g, nullptr, nullptr) : 0;
+    const int grid = static_cast<int>(grid_for((n - head) / 4 + 1, U, resident));
+    f.total_blocks = grid;
+    norm_kernel<U><<<grid, kThreads, 0, as_stream(stream)>>>(g, n, head, f);
+    return check_launch(what);
+}
+
+// SS_NORM_UNROLL overrides the K1 unroll for tuning sweeps
+int launch_norm(const float* g, int64_t n, const Finish& f, void* stream, const char* what) {
+    static int u = -1;
+    if (u < 0) {
+        const char* e = getenv("SS_NORM_UNROLL");
+        u = e ? atoi(e) : 0;
+    }
+    switch (u) {
+        case 1: return launch_norm_u<1>(g, n, f, stream, what);
+        case 2: return launch_norm_u<2>(g, n, f, stream, what);
+        case 4: return launch_norm_u<4>(g, n, f, stream, what);
+        case 8: return launch_norm_u<8>(g, n, f, stream, what);
+        default: return launch_norm_u<kNormUnroll>(g, n, f, stream, what);
+    }
+}
+
 }  // namespace
 
 namespace ss_internal {
@@ -702,13 +766,8 @@ int ss_workspace_reset(void* ws, void* stream) {
 int ss_norm_sq_f32(const float* g, int64_t n, double* out, void* ws, void* stream) {
     if (n < 0) return fail(SS_ERR_CONFIG, "n must be >= 0, got %lld", (long long)n);
     if ((n > 0 && !g) || !out || !ws) return fail(SS_ERR_CONFIG, "null pointer argument");
-    constexpr int U = 4;
-    static const int resident = resident_blocks(norm_kernel<U>);
-    const int64_t head = n ? common_head(n, g, nullptr, nullptr) : 0;
-    const int grid = static_cast<int>(grid_for((n - head) / 4 + 1, U, resident));
-    Finish f{ws, 0, grid, out, nullptr, 0.0, nullptr, nullptr, 0};
-    norm_kernel<U><<<grid, kThreads, 0, as_stream(stream)>>>(g, n, head, f);
-    return check_launch("ss_norm_sq_f32");
+    Finish f{ws, 0, 0, out, nullptr, 0.0, nullptr, nullptr, 0};
+    return launch_norm(g, n, f, stream, "ss_norm_sq_f32");
 }
 
 int ss_norm_sq_multi_f32(const float* const* ptrs, const int64_t* sizes, int32_t count, double* out,
@@ -787,28 +846,60 @@ int ss_norm_signal_f32(const float* g, int64_t n, ss_signal_state* st, double de
     if (rc) return rc;
     rc = check_trace(trace, cap);
     if (rc) return rc;
-    constexpr int U = 4;
-    static const int resident = resident_blocks(norm_kernel<U>);
-    const int64_t head = n ? common_head(n, g, nullptr, nullptr) : 0;
-    const int grid = static_cast<int>(grid_for((n - head) / 4 + 1, U, resident));
-    Finish f{ws, 0, grid, nullptr, st, delta, word, trace, cap};
-    norm_kernel<U><<<grid, kThreads, 0, as_stream(stream)>>>(g, n, head, f);
-    return check_launch("ss_norm_signal_f32");
+    Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
+    return launch_norm(g, n, f, stream, "ss_norm_signal_f32");
 }
 
 }  // extern "C"
 
 namespace {
 
-template <bool MOM, bool NEST, bool NORM>
-int launch_sgd(const SgdArgs& a, const Finish& f0, void* stream) {
-    constexpr int U = MOM ? 2 : 4;
-    static const int resident = resident_blocks(sgd_kernel<MOM, NEST, NORM, U>);
+template <bool MOM, bool NEST, bool NORM, int U, int CP>
+int launch_sgd_v(const SgdArgs& a, const Finish& f0, void* stream) {
+    static const int resident = resident_blocks(sgd_kernel<MOM, NEST, NORM, U, CP>);
     const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, U, resident));
     Finish f = f0;
     f.total_blocks = grid;
-    sgd_kernel<MOM, NEST, NORM, U><<<grid, kThreads, 0, as_stream(stream)>>>(a, f);
+    sgd_kernel<MOM, NEST, NORM, U, CP><<<grid, kThreads, 0, as_stream(stream)>>>(a, f);
     return check_launch(NORM ? "ss_update_norm_signal_f32" : "ss_sgd_update_f32");
+}
+
+// SS_SGD_VARIANT="<cp><u>" (e.g. "21") overrides the cache policy / unroll of
+// the momentum K13 kernel for tuning sweeps (tools/sgd_sweep.py); unset = default
+// measured at P = 100M (tools/sgd_sweep.py): momentum (3 streams) U=1 6.40 TB/s vs U=2 5.92,
+// U=4 5.67; plain (2 streams) U=2 6.23 vs U=1 6.01
+template <bool MOM>
+constexpr int kSgdUnroll = MOM ? 1 : 2;
+
+int sgd_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("SS_SGD_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <bool MOM, bool NEST, bool NORM>
+int launch_sgd(const SgdArgs& a, const Finish& f0, void* stream) {
+    if constexpr (!NEST) {
+        switch (sgd_variant()) {
+            case 1: return launch_sgd_v<MOM, NEST, NORM, 1, 0>(a, f0, stream);
+            case 4: return launch_sgd_v<MOM, NEST, NORM, 4, 0>(a, f0, stream);
+            case 11: return launch_sgd_v<MOM, NEST, NORM, 1, 1>(a, f0, stream);
+            case 12: return launch_sgd_v<MOM, NEST, NORM, 2, 1>(a, f0, stream);
+            case 14: return launch_sgd_v<MOM, NEST, NORM, 4, 1>(a, f0, stream);
+            case 21: return launch_sgd_v<MOM, NEST, NORM, 1, 2>(a, f0, stream);
+            case 22: return launch_sgd_v<MOM, NEST, NORM, 2, 2>(a, f0, stream);
+            case 24: return launch_sgd_v<MOM, NEST, NORM, 4, 2>(a, f0, stream);
+            case 31: return launch_sgd_v<MOM, NEST, NORM, 1, 3>(a, f0, stream);
+            case 32: return launch_sgd_v<MOM, NEST, NORM, 2, 3>(a, f0, stream);
+            case 34: return launch_sgd_v<MOM, NEST, NORM, 4, 3>(a, f0, stream);
+            case 2: return launch_sgd_v<MOM, NEST, NORM, 2, 0>(a, f0, stream);
+            default: break;
+        }
+    }
+    return launch_sgd_v<MOM, NEST, NORM, kSgdUnroll<MOM>, 0>(a, f0, stream);
 }
 
 template <bool NORM>
@@ -957,8 +1048,7 @@ int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, void* stream) {
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, avg_kernel<W>, 512, 0) != cudaSuccess || x <= 0) x = 1;
         avg_resident = x;
     }
-    constexpr int U = MOM ? 2 : 4;
-    const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, U, resident));
+    const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, resident));
     f.total_blocks = grid;
     // averaging grid: every block co-resident (the last one runs the end barrier)
     int avg_grid = sm_count() * avg_resident;

@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kThreads = 512;
 
-template <int W>
+template <int W, int UO = 0>
 __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     __shared__ int s_word;
     __shared__ bool s_timeout;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     const int w = s_word;
     const bool sync = !s_timeout && w == SS_FLAG_SYNC;
     if (sync) {
-        average_shard<W>(a);
+        average_shard<W, UO>(a);
         __threadfence_system();
     }
     __syncthreads();
@@ -93,12 +93,12 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     }
 }
 
-template <int W>
-int launch_symm(const SymmArgs& a, cudaStream_t s) {
+template <int W, int UO = 0>
+int launch_symm_u(const SymmArgs& a, cudaStream_t s) {
     static int resident = 0;
     if (resident == 0) {
         int x = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, symm_sync_kernel<W>, kThreads, 0) != cudaSuccess || x <= 0) x = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, symm_sync_kernel<W, UO>, kThreads, 0) != cudaSuccess || x <= 0) x = 1;
         resident = x;
     }
     // all blocks co-resident: they never wait on each other, but the last
@@ -113,8 +113,29 @@ int launch_symm(const SymmArgs& a, cudaStream_t s) {
     const int64_t per_rank_vec = ((a.n >> 2) + a.world - 1) / a.world;
     const int64_t want = (per_rank_vec + kThreads * 4 - 1) / (kThreads * 4);
     if (want < grid) grid = static_cast<int>(want < 1 ? 1 : want);
-    symm_sync_kernel<W><<<grid, kThreads, 0, s>>>(a);
+    symm_sync_kernel<W, UO><<<grid, kThreads, 0, s>>>(a);
     return ss_internal::check_launch("ss_symm_sync_f32");
+}
+
+// SS_SYMM_UNROLL overrides the vectors-in-flight per thread of the mean
+// (tuning sweeps, tools/symm_perf.py); widths 0 (NVLS), 2, 4, 8 only
+template <int W>
+int launch_symm(const SymmArgs& a, cudaStream_t s) {
+    static int u = -1;
+    if (u < 0) {
+        const char* e = getenv("SS_SYMM_UNROLL");
+        u = e ? atoi(e) : 0;
+    }
+    if constexpr (W == 0 || W == 2 || W == 4 || W == 8) {
+        switch (u) {
+            case 1: return launch_symm_u<W, 1>(a, s);
+            case 2: return launch_symm_u<W, 2>(a, s);
+            case 4: return launch_symm_u<W, 4>(a, s);
+            case 8: return launch_symm_u<W, 8>(a, s);
+            default: break;
+        }
+    }
+    return launch_symm_u<W, 0>(a, s);
 }
 
 }  // namespace

@@ -101,7 +101,7 @@ __device__ __forceinline__ void shard_range(const SymmArgs& a, int64_t* v0, int6
 // NVLS: the switch reduces, multimem.st broadcasts (W = 0) -- or P2P two-shot
 // over W peers: all W loads of U vectors issued before any add (fixed rank
 // order => every rank's copy of a shard is bit-identical).
-template <int W>
+template <int W, int UO = 0>
 __device__ void average_shard(const SymmArgs& a) {
     int64_t v0, v1;
     shard_range(a, &v0, &v1);
@@ -110,7 +110,7 @@ __device__ void average_shard(const SymmArgs& a) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     int64_t i = v0 + tid;
     if constexpr (W == 0) {
-        constexpr int U = 4;
+        constexpr int U = UO ? UO : 4;
         for (; i + (U - 1) * stride < v1; i += U * stride) {
             float4 v[U];
 #pragma unroll
@@ -124,7 +124,7 @@ __device__ void average_shard(const SymmArgs& a) {
                 mm_st1(a.mc + j, mm_ld_reduce_add1(a.mc + j) * a.scale);
         }
     } else {
-        constexpr int U = W <= 2 ? 4 : (W <= 4 ? 2 : 1);
+        constexpr int U = UO ? UO : (W <= 2 ? 4 : (W <= 4 ? 2 : 1));
         const float4* src[W];
         float4* dst[W];
 #pragma unroll

@@ -72,6 +72,10 @@ for mc in (True, False):  # explicit choice per path
     if rank == 0:
         print(f"    p2p flag exchange, local: {ms * 1e3:.1f} us", flush=True)
 
+if os.environ.get("SYMM_ONLY"):
+    dist.barrier(device_ids=[local])
+    dist.destroy_process_group()
+    sys.exit(0)
 buf = torch.randn(P, device=dev)
 report("nccl all_reduce AVG", timeit(lambda: dist.all_reduce(buf, op=dist.ReduceOp.AVG)))
 report("nccl all_reduce SUM", timeit(lambda: dist.all_reduce(buf, op=dist.ReduceOp.SUM)))
