@@ -15,8 +15,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRCS = [PKG / "csrc" / "selsync_b200.cu", PKG / "csrc" / "selsync_symm.cu"]
-DEPS = [*SRCS, PKG / "csrc" / "common.cuh"]
+SRCS = [PKG / "csrc" / f for f in ("selsync_b200.cu", "selsync_symm.cu", "selsync_step.cu")]
+DEPS = [*SRCS, *sorted((PKG / "csrc").glob("*.cuh"))]
 HEADER = ROOT / "include" / "selsync_b200.h"
 OUT = PKG / "_lib" / "libselsync_b200.so"
 
