@@ -64,6 +64,8 @@ def parse():
                     help="C2 back end at N > 1: device-conditional symmetric-memory kernel or host-branch NCCL")
     ap.add_argument("--flag-exchange", default="p2p", choices=["p2p", "fused", "nccl"],
                     help="fused: the whole step in one cooperative launch (symm only)")
+    ap.add_argument("--order", default="update_first", choices=["update_first", "norm_first", "adaptive"],
+                    help="one-launch step order (flag-exchange fused): norm_first overlaps update and mean")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
@@ -226,6 +228,7 @@ def workload_config(args, world):
         "order": "prescale" if args.no_fuse else "fused",
         "collective": args.collective if world > 1 else "none (single rank)",
         "flag_exchange": args.flag_exchange if world > 1 else "none (single rank)",
+        "step_order": args.order if world > 1 and args.flag_exchange == "fused" else "update_first",
         "decision_mix": {"sync_frac": 0.5, "grad_scales": MIX_SCALES, "smoothing": 1.0, "delta": 0.3,
                          "warmup": 1},
         "parallelism": f"dp{world} (SelSync replicas, NCCL)",
@@ -280,7 +283,7 @@ def main():
         st = SelSyncStep(w, g, cfg, momentum_buffer=mom, group=comm, fuse=not args.no_fuse,
                          collective=args.collective if world > 1 else None,
                          flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
-                         trace_capacity=1 << 14, profile=True)
+                         trace_capacity=1 << 14, profile=True, order=args.order)
         return st
 
     def run(step, n, host_ring=None, host_row=None):
@@ -359,6 +362,8 @@ def main():
     bytes_per_launch = (20 if args.momentum else 12) * P
     if args.no_fuse:
         bytes_per_launch = 4 * P
+    if one_launch and args.order == "norm_first":
+        bytes_per_launch += 4 * P  # norm pass first, then the plain update (both inside the launch)
     achieved = bytes_per_launch / (k_mean * 1e-3) / 1e9
     kernel_name = ("ss_update_norm_signal_f32 (K13+K2: fused SGD-momentum-wd update + ||g||^2 + signal step)"
                    if not args.no_fuse else "ss_norm_signal_f32 (K1+K2)")

@@ -189,6 +189,20 @@ typedef struct ss_symm_group {
     int32_t world;
     int32_t ring_cap;
     int32_t reserved;
+    /* order of the one-launch step (ss_step_symm_f32):
+         0  update first: K13 (update + ||g||^2) then, on sync, the mean;
+         1  norm first: K1, vote, then on sync ONE kernel that overlaps the update
+            of each tile with the NVLink mean of tiles all ranks have finished
+            (on local steps the plain update);
+         2  adaptive: order 1 while an EWMA of the agreed decisions >= threshold.
+       Both orders compute identical parameters. Order 1/2 needs the fields below. */
+    int32_t order_mode;
+    float order_threshold;
+    uint32_t* tile_cnt[SS_SYMM_MAX_RANKS]; /* rank r's per-tile arrival counters (peer-mapped, zeroed) */
+    uint32_t* epoch;                    /* overlapped sync steps completed (zeroed) */
+    float* predictor;                   /* EWMA of agreed sync decisions (zeroed) */
+    int64_t tile_elems;                 /* elements per tile, multiple of 4 */
+    int64_t n_tiles;                    /* capacity of every tile_cnt array */
 } ss_symm_group;
 
 /* bytes of each rank's signal region (flag slots + done slots, uint64 each) */

@@ -80,6 +80,13 @@ class SymmGroupC(Structure):
         ("world", c_int32),
         ("ring_cap", c_int32),
         ("reserved", c_int32),
+        ("order_mode", c_int32),
+        ("order_threshold", c_float),
+        ("tile_cnt", c_void_p * SYMM_MAX_RANKS),
+        ("epoch", c_void_p),
+        ("predictor", c_void_p),
+        ("tile_elems", c_int64),
+        ("n_tiles", c_int64),
     ]
 
 

@@ -105,8 +105,11 @@ class SymmetricParams:
     loads/stores otherwise), with no host involvement.
     """
 
+    ORDERS = {"update_first": 0, "norm_first": 1, "adaptive": 2}
+
     def __init__(self, numel: int, device, comm: RankGroup, *, ring_capacity: int = 1 << 14,
-                 timeout_s: float = 30.0, use_multicast="auto"):
+                 timeout_s: float = 30.0, use_multicast="auto", order: str = "update_first",
+                 order_threshold: float = 0.3, tile_elems: int = 16384):
         import ctypes
 
         import torch.distributed._symmetric_memory as symm_mem
@@ -155,6 +158,27 @@ class SymmetricParams:
         g.err = self.err.data_ptr()
         g.timeout_s = self.timeout_s
         g.rank, g.world, g.ring_cap = self.rank, self.world, self.ring_capacity
+        # order of the one-launch step; the norm-first order overlaps the update
+        # with the mean on sync steps and needs per-tile arrival counters
+        if order not in self.ORDERS:
+            raise ConfigError(f"order must be one of {sorted(self.ORDERS)}, got {order!r}")
+        if tile_elems <= 0 or tile_elems % 4:
+            raise ConfigError("tile_elems must be a positive multiple of 4")
+        self.order = order
+        g.order_mode = self.ORDERS[order]
+        g.order_threshold = float(order_threshold)
+        self.n_tiles = (numel + tile_elems - 1) // tile_elems
+        self.cnt = symm_mem.empty(max(1, self.n_tiles), dtype=torch.int32, device=self.device)
+        self.cnt_hdl = symm_mem.rendezvous(self.cnt, group)
+        self.cnt.zero_()
+        for r, p in enumerate(self.cnt_hdl.buffer_ptrs):
+            g.tile_cnt[r] = int(p)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.predictor = torch.zeros(1, dtype=torch.float32, device=self.device)
+        g.epoch = self.epoch.data_ptr()
+        g.predictor = self.predictor.data_ptr()
+        g.tile_elems = int(tile_elems)
+        g.n_tiles = int(self.n_tiles)
         self.group_c = g
         self.group_ref = ctypes.byref(g)
         torch.cuda.synchronize(self.device)

@@ -252,6 +252,30 @@ __device__ void finish_norm(const Finish& f, double acc) {
     }
 }
 
+// ---------------------------------------------------------------- K1 pass
+
+// this thread's fp64 partial of ||g||^2 over a grid-stride sweep
+template <int U>
+__device__ __forceinline__ double norm_pass(const float* __restrict__ g, int64_t n, int64_t head) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    double acc = 0.0;
+    for (int64_t i = tid; i < head; i += stride) acc = fma((double)g[i], (double)g[i], acc);
+    const float* gb = g + head;
+    const int64_t nvec = (n - head) >> 2;
+    int64_t i = tid;
+    for (; i + (U - 1) * stride < nvec; i += U * stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_cs4(gb + 4 * (i + u * stride));
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = sq4(v[u], acc);
+    }
+    for (; i < nvec; i += stride) acc = sq4(ld_cs4(gb + 4 * i), acc);
+    for (int64_t j = head + 4 * nvec + tid; j < n; j += stride) acc = fma((double)g[j], (double)g[j], acc);
+    return acc;
+}
+
 // ---------------------------------------------------------------- K3 / K13
 
 struct SgdArgs {
@@ -342,6 +366,34 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
         if (MOM) a.m[j] = m;
     }
     return acc;
+}
+
+// The update over elements [e0, e1) by the threads of ONE block (tile work of
+// the overlapped sync step). Requires 16-byte-aligned streams (head == 0) and
+// e0 % 4 == 0; a scalar tail is handled when e1 is not a multiple of 4.
+template <bool MOM, bool NEST>
+__device__ __forceinline__ void sgd_block_range(const SgdArgs& a, int64_t e0, int64_t e1) {
+    const float s = 1.0f;
+    const int64_t v0 = e0 >> 2, v1 = e1 >> 2;
+    for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+        const int64_t k = 4 * i;
+        float4 gv = ld_cs4(a.g + k), wv = ld_cs4(a.w + k);
+        float4 mm = MOM ? ld_cs4(a.m + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        sgd_elem<MOM, NEST>(wv.x, gv.x, mm.x, a, s);
+        sgd_elem<MOM, NEST>(wv.y, gv.y, mm.y, a, s);
+        sgd_elem<MOM, NEST>(wv.z, gv.z, mm.z, a, s);
+        sgd_elem<MOM, NEST>(wv.w, gv.w, mm.w, a, s);
+        st_cs4(a.w + k, wv);
+        if (MOM) st_cs4(a.m + k, mm);
+    }
+    float mdummy = 0.0f;
+    for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x) {
+        float w = a.w[j], g = a.g[j];
+        float m = MOM ? a.m[j] : 0.0f;
+        sgd_elem<MOM, NEST>(w, g, MOM ? m : mdummy, a, s);
+        a.w[j] = w;
+        if (MOM) a.m[j] = m;
+    }
 }
 
 }  // namespace

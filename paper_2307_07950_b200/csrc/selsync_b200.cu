@@ -60,23 +60,7 @@ int check_launch(const char* what) {
 template <int U>
 __global__ void __launch_bounds__(kThreads, 4) norm_kernel(const float* __restrict__ g, int64_t n,
                                                         int64_t head, Finish f) {
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    double acc = 0.0;
-    for (int64_t i = tid; i < head; i += stride) acc = fma((double)g[i], (double)g[i], acc);
-    const float* gb = g + head;
-    const int64_t nvec = (n - head) >> 2;
-    int64_t i = tid;
-    for (; i + (U - 1) * stride < nvec; i += U * stride) {
-        float4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = ld_cs4(gb + 4 * (i + u * stride));
-#pragma unroll
-        for (int u = 0; u < U; ++u) acc = sq4(v[u], acc);
-    }
-    for (; i < nvec; i += stride) acc = sq4(ld_cs4(gb + 4 * i), acc);
-    for (int64_t j = head + 4 * nvec + tid; j < n; j += stride) acc = fma((double)g[j], (double)g[j], acc);
-    finish_norm(f, acc);
+    finish_norm(f, norm_pass<U>(g, n, head));
 }
 
 // ---------------------------------------------------------------- K2

@@ -2,9 +2,31 @@
 //
 // Reference path (/root/reference/pkg/src/selsync): _selsync_step
 // (strategies.py:369-403) with the parameter server's flag relay
-// (runtime.py:319-333) and mean round (runtime.py:275-294). On the device:
-// update + ||g||^2 + signal (K13+K2) -> vote exchange over NVLink (C1) ->
-// on sync only, a dynamically launched NVLink mean (C2).
+// (runtime.py:319-333) and mean round (runtime.py:275-294).
+//
+// step_kernel (one host launch per step) runs one of two orders, chosen on
+// the device so every rank takes the same one:
+//
+//  update first (order 0): K13 -- update + ||g||^2 over the whole buffer; the
+//     last block to arrive reduces the partials, runs K2, posts its vote to
+//     every peer's signal slot and waits for the N votes (C1: MAX = OR); every
+//     other block has already exited. On sync it tail-launches avg_kernel
+//     (CUDA dynamic parallelism, cudaStreamTailLaunch) -- the NVLink mean of
+//     this rank's shard with the 1/N in the epilogue (C2) + end barrier.
+//     20P HBM bytes; a sync step pays update + mean back to back.
+//
+//  norm first (order 1): K1 -- ||g||^2 only (4P); vote exchange as above;
+//     then on a local step the plain update (20P) and on a sync step
+//     upd_avg_kernel, which OVERLAPS the HBM-bound update with the
+//     NVLink-bound mean tile by tile: blocks pull tickets in a fixed order
+//     (N update tiles, then the mean of one tile this rank owns that was
+//     updated `lag` groups earlier); a rank announces a finished tile by a
+//     remote atomic add on the owner's counter, the owner reduces the tile
+//     once all N counts are in. A sync step then costs ~max(update, mean).
+//
+//  adaptive (order 2): the last block keeps an EWMA of the agreed decisions;
+//     the next step uses order 1 while it is >= threshold. Both orders
+//     compute identical parameters (same per-element arithmetic).
 
 #include "selsync_b200.h"
 #include "common.cuh"
@@ -15,42 +37,134 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 using ss_internal::check_launch;
 using ss_internal::fail;
 
 namespace {
 
-// ------------------------------------------- the whole step in one host launch
-//
-// step_kernel: K13 (update + ||g||^2) over the whole buffer; the last block
-// to arrive reduces the partials, runs K2, posts its vote to every peer's
-// signal slot and waits for the N votes (C1: MAX = OR). Every other block has
-// already exited, so a local step costs the update plus one NVLink round trip
-// in a single block. On sync the last block tail-launches avg_kernel (CUDA
-// dynamic parallelism, cudaStreamTailLaunch: it starts once this grid has
-// fully retired) which averages this rank's shard over NVLink with the 1/N in
-// the epilogue (C2) and closes with the end barrier. One host launch per step,
-// the branch never leaves the device.
+struct OverlapArgs {
+    uint32_t* cnt[kMaxRanks];  // per-rank tile arrival counters, indexed by tile
+    uint32_t* epoch;
+    float* predictor;
+    int mode;
+    float threshold;
+    int64_t tile;
+    int64_t n_tiles;
+    int lag;                   // groups between an update ticket and the owner's mean ticket
+    unsigned long long* ticket;
+};
+
+struct Grids {
+    int avg;   // avg_kernel
+    int upd;   // plain update (order 1, local steps)
+    int ua;    // upd_avg_kernel
+};
+
+__device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// end of a sync step on this rank: done tags to every peer, wait for all
+__device__ void end_barrier(const SymmArgs& s, uint64_t seq) {
+    for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.world + s.rank, seq);
+    bool to = false;
+    for (int j = 0; j < s.world && !to; ++j) wait_tag(s.pads[s.rank] + s.world + j, seq, 0, s, &to);
+    if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+}
+
 template <int W>
 __global__ void __launch_bounds__(512, 2) avg_kernel(SymmArgs s, uint64_t seq) {
     average_shard<W>(s);
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
-        for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.world + s.rank, seq);
-        bool to = false;
-        for (int j = 0; j < s.world && !to; ++j) wait_tag(s.pads[s.rank] + s.world + j, seq, 0, s, &to);
-        if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+        end_barrier(s, seq);
+        *s.arrive = 0u;
+        *s.seq = static_cast<uint32_t>(seq);
+    }
+}
+
+template <bool MOM, bool NEST>
+__global__ void __launch_bounds__(kThreads, 4) update_kernel(SgdArgs a) {
+    sgd_pass<MOM, NEST, false, (MOM ? 1 : 2)>(a);
+}
+
+template <bool MOM, bool NEST, int W>
+__global__ void __launch_bounds__(kThreads, 4) upd_avg_kernel(SgdArgs a, SymmArgs s, OverlapArgs o,
+                                                               uint64_t seq, uint32_t epoch) {
+    __shared__ unsigned long long s_ticket;
+    const int N = s.world;
+    const int64_t groups = (o.n_tiles + N - 1) / N + o.lag;
+    const unsigned long long total = static_cast<unsigned long long>(groups) * (N + 1);
+    const uint32_t target = static_cast<uint32_t>(N) * epoch;
+    for (;;) {
+        if (threadIdx.x == 0) s_ticket = atomicAdd(o.ticket, 1ull);
+        __syncthreads();
+        const unsigned long long k = s_ticket;
+        __syncthreads();
+        if (k >= total) break;
+        const int64_t grp = static_cast<int64_t>(k / (N + 1));
+        const int pos = static_cast<int>(k % (N + 1));
+        if (pos < N) {
+            const int64_t t = grp * N + pos;  // update tile t (owner t % N)
+            if (t < o.n_tiles) {
+                const int64_t e0 = t * o.tile;
+                const int64_t e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
+                sgd_block_range<MOM, NEST>(a, e0, e1);
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence_system();
+                    red_add_release_sys(o.cnt[t % N] + t, 1u);
+                }
+            }
+        } else {
+            const int64_t m = grp - o.lag;
+            const int64_t t = m * N + s.rank;  // mean of owned tile t once all N ranks updated it
+            if (m >= 0 && t < o.n_tiles) {
+                if (threadIdx.x == 0) {
+                    const uint64_t t0 = now_ns();
+                    while (static_cast<int32_t>(ld_acquire_sys_u32(o.cnt[s.rank] + t) - target) < 0) {
+                        if (now_ns() - t0 > s.timeout_ns) {
+                            atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+                            break;
+                        }
+                        __nanosleep(128);
+                    }
+                }
+                __syncthreads();
+                const int64_t e0 = t * o.tile;
+                const int64_t e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
+                average_block_range<W>(s, e0, e1);
+            }
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+        end_barrier(s, seq);
+        *o.ticket = 0ull;
+        *o.epoch = epoch;
         *s.arrive = 0u;
         *s.seq = static_cast<uint32_t>(seq);
     }
 }
 
 template <bool MOM, bool NEST, int W>
-__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, int avg_grid) {
+__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o,
+                                                            Grids gr) {
     __shared__ bool s_last;
-    const double acc = sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
+    // the order of this step: identical on every rank (same decision history)
+    const bool norm_first = o.mode == 1 || (o.mode == 2 && *reinterpret_cast<volatile float*>(o.predictor) >= o.threshold);
+    const double acc = norm_first ? norm_pass<4>(a.g, a.n, a.head)
+                                  : sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
     Workspace ws = ws_view(f.ws);
     const double bsum = block_sum(acc);
     if (threadIdx.x == 0) {
@@ -84,45 +198,62 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
     }
     *f.word = w;
     if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
-    if (w == SS_FLAG_SYNC) {
-        avg_kernel<W><<<avg_grid, 512, 0, cudaStreamTailLaunch>>>(s, seq);
+    const bool sync = w == SS_FLAG_SYNC;
+    if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (sync ? 0.25f : 0.0f);
+    if (norm_first) {
+        if (sync) {
+            upd_avg_kernel<MOM, NEST, W><<<gr.ua, kThreads, 0, cudaStreamTailLaunch>>>(a, s, o, seq, *o.epoch + 1);
+        } else {
+            update_kernel<MOM, NEST><<<gr.upd, kThreads, 0, cudaStreamTailLaunch>>>(a);
+            *s.seq = static_cast<uint32_t>(seq);
+        }
+    } else if (sync) {
+        avg_kernel<W><<<gr.avg, 512, 0, cudaStreamTailLaunch>>>(s, seq);
     } else {
         *s.seq = static_cast<uint32_t>(seq);
     }
 }
 
-}  // namespace
-
-namespace {
+template <typename K>
+int occupancy(K kernel, int threads) {
+    int x = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, kernel, threads, 0) != cudaSuccess || x <= 0) x = 1;
+    return x;
+}
 
 template <bool MOM, bool NEST, int W>
-int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, void* stream) {
-    static int resident = 0, avg_resident = 0;
-    if (resident == 0) {
-        int x = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, step_kernel<MOM, NEST, W>, kThreads, 0) != cudaSuccess || x <= 0)
-            x = 1;
-        resident = x;
-        x = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, avg_kernel<W>, 512, 0) != cudaSuccess || x <= 0) x = 1;
-        avg_resident = x;
+int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, void* stream) {
+    static int res_step = 0, res_avg = 0, res_upd = 0, res_ua = 0;
+    if (res_step == 0) {
+        res_step = occupancy(step_kernel<MOM, NEST, W>, kThreads);
+        res_avg = occupancy(avg_kernel<W>, 512);
+        res_upd = occupancy(update_kernel<MOM, NEST>, kThreads);
+        res_ua = occupancy(upd_avg_kernel<MOM, NEST, W>, kThreads);
     }
-    const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, resident));
+    const int sms = ss_internal::sm_count();
+    const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res_step));
     f.total_blocks = grid;
+    Grids gr;
     // averaging grid: every block co-resident (the last one runs the end barrier)
-    int avg_grid = ss_internal::sm_count() * avg_resident;
+    gr.avg = sms * res_avg;
     const int64_t per_rank_vec = ((sa.n >> 2) + sa.world - 1) / sa.world;
     const int64_t want = (per_rank_vec + 512 * 4 - 1) / (512 * 4);
-    if (want < avg_grid) avg_grid = static_cast<int>(want < 1 ? 1 : want);
-    step_kernel<MOM, NEST, W><<<grid, kThreads, 0, as_stream(stream)>>>(a, f, sa, avg_grid);
+    if (want < gr.avg) gr.avg = static_cast<int>(want < 1 ? 1 : want);
+    gr.upd = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res_upd));
+    gr.ua = sms * res_ua;
+    if (o.n_tiles * 2 < gr.ua) gr.ua = static_cast<int>(o.n_tiles * 2 > 0 ? o.n_tiles * 2 : 1);
+    // in-flight window ~ gr.ua tickets = gr.ua / (N + 1) groups: lag one window past it
+    o.lag = gr.ua / (sa.world + 1) + 2;
+    step_kernel<MOM, NEST, W><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, f, sa, o, gr);
     return check_launch("ss_step_symm_f32");
 }
 
 template <int W>
-int dispatch_step(const SgdArgs& a, const Finish& f, const SymmArgs& sa, bool mom, bool nest, void* stream) {
-    if (!mom) return launch_step<false, false, W>(a, f, sa, stream);
-    if (nest) return launch_step<true, true, W>(a, f, sa, stream);
-    return launch_step<true, false, W>(a, f, sa, stream);
+int dispatch_step(const SgdArgs& a, const Finish& f, const SymmArgs& sa, const OverlapArgs& o, bool mom,
+                  bool nest, void* stream) {
+    if (!mom) return launch_step<false, false, W>(a, f, sa, o, stream);
+    if (nest) return launch_step<true, true, W>(a, f, sa, o, stream);
+    return launch_step<true, false, W>(a, f, sa, o, stream);
 }
 
 }  // namespace
@@ -145,13 +276,33 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
                               &ss_internal::fail);
     if (rc) return rc;
     if (grp->bufs[grp->rank] != w) return fail(SS_ERR_CONFIG, "w must be this rank's symmetric buffer");
+    OverlapArgs o{};
+    o.mode = grp->order_mode;
+    o.threshold = grp->order_threshold;
+    if (o.mode < 0 || o.mode > 2) return fail(SS_ERR_CONFIG, "order_mode must be 0, 1 or 2, got %d", o.mode);
+    if (o.mode != 0) {
+        if (a.head != 0) return fail(SS_ERR_CONFIG, "norm-first order needs 16-byte aligned w, g, m");
+        if (!grp->epoch || !grp->predictor || grp->tile_elems <= 0 || (grp->tile_elems & 3))
+            return fail(SS_ERR_CONFIG, "norm-first order needs epoch, predictor and a tile size (multiple of 4)");
+        const int64_t tiles = (n + grp->tile_elems - 1) / grp->tile_elems;
+        if (tiles > grp->n_tiles) return fail(SS_ERR_CONFIG, "tile counters hold %lld tiles, need %lld",
+                                             (long long)grp->n_tiles, (long long)tiles);
+        for (int r = 0; r < grp->world; ++r)
+            if (!grp->tile_cnt[r]) return fail(SS_ERR_CONFIG, "null tile counters for rank %d", r);
+        for (int r = 0; r < kMaxRanks; ++r) o.cnt[r] = r < grp->world ? grp->tile_cnt[r] : nullptr;
+        o.epoch = grp->epoch;
+        o.predictor = grp->predictor;
+        o.tile = grp->tile_elems;
+        o.n_tiles = tiles;
+        o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
+    }
     Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
     const bool mom = momentum != 0.0f, nest = nesterov != 0;
     switch (symm_width(sa)) {
-        case 0: return dispatch_step<0>(a, f, sa, mom, nest, stream);
-        case 2: return dispatch_step<2>(a, f, sa, mom, nest, stream);
-        case 4: return dispatch_step<4>(a, f, sa, mom, nest, stream);
-        case 8: return dispatch_step<8>(a, f, sa, mom, nest, stream);
+        case 0: return dispatch_step<0>(a, f, sa, o, mom, nest, stream);
+        case 2: return dispatch_step<2>(a, f, sa, o, mom, nest, stream);
+        case 4: return dispatch_step<4>(a, f, sa, o, mom, nest, stream);
+        case 8: return dispatch_step<8>(a, f, sa, o, mom, nest, stream);
         default:
             return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 2, 4, 8)", sa.world);
     }

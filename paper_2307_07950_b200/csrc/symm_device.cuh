@@ -90,6 +90,47 @@ __device__ __forceinline__ float4 scale4(float4 v, float s) {
     return v;
 }
 
+// Mean over ranks of elements [e0, e1) by the threads of ONE block (tile work
+// of the overlapped sync step); e0 % 4 == 0, scalar tail when e1 % 4 != 0.
+template <int W>
+__device__ void average_block_range(const SymmArgs& a, int64_t e0, int64_t e1) {
+    const int64_t v0 = e0 >> 2, v1 = e1 >> 2;
+    if constexpr (W == 0) {
+        int64_t i = v0 + threadIdx.x;
+        for (; i + blockDim.x < v1; i += 2 * blockDim.x) {
+            float4 x = mm_ld_reduce_add4(a.mc + 4 * i);
+            float4 y = mm_ld_reduce_add4(a.mc + 4 * (i + blockDim.x));
+            mm_st4(a.mc + 4 * i, scale4(x, a.scale));
+            mm_st4(a.mc + 4 * (i + blockDim.x), scale4(y, a.scale));
+        }
+        for (; i < v1; i += blockDim.x) mm_st4(a.mc + 4 * i, scale4(mm_ld_reduce_add4(a.mc + 4 * i), a.scale));
+        for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x)
+            mm_st1(a.mc + j, mm_ld_reduce_add1(a.mc + j) * a.scale);
+    } else {
+        for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+            float4 v[W];
+#pragma unroll
+            for (int r = 0; r < W; ++r) v[r] = __ldcg(reinterpret_cast<const float4*>(a.bufs[r]) + i);
+            float4 acc = v[0];
+#pragma unroll
+            for (int r = 1; r < W; ++r) {
+                acc.x += v[r].x; acc.y += v[r].y; acc.z += v[r].z; acc.w += v[r].w;
+            }
+            acc = scale4(acc, a.scale);
+#pragma unroll
+            for (int r = 0; r < W; ++r) __stcg(reinterpret_cast<float4*>(a.bufs[r]) + i, acc);
+        }
+        for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x) {
+            float acc = __ldcg(a.bufs[0] + j);
+#pragma unroll
+            for (int r = 1; r < W; ++r) acc += __ldcg(a.bufs[r] + j);
+            acc *= a.scale;
+#pragma unroll
+            for (int r = 0; r < W; ++r) __stcg(a.bufs[r] + j, acc);
+        }
+    }
+}
+
 // Shard of rank r: vectors [v0, v1) of the n/4 float4s; the scalar tail goes to the last rank.
 __device__ __forceinline__ void shard_range(const SymmArgs& a, int64_t* v0, int64_t* v1) {
     const int64_t nvec = a.n >> 2;

@@ -58,6 +58,8 @@ class SelSyncStep:
         broadcast_init: bool = True,
         profile: bool = False,
         timeout_s: float = 30.0,
+        order: str = "update_first",
+        order_threshold: float = 0.3,
     ):
         if not isinstance(config, SelSyncConfig):
             raise ConfigError("config must be a SelSyncConfig")
@@ -100,7 +102,8 @@ class SelSyncStep:
         self.symm = None
         if self.collective == "symm":
             self.symm = SymmetricParams(params.numel(), self.device, self.comm,
-                                        ring_capacity=trace_capacity, timeout_s=timeout_s)
+                                        ring_capacity=trace_capacity, timeout_s=timeout_s,
+                                        order=order, order_threshold=order_threshold)
             self.symm.buf.copy_(params)
             params = self.symm.buf  # the step owns the symmetric copy; use step.params
             if self.flag_exchange == "fused" and not self.symm.one_launch_capable:

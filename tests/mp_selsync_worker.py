@@ -29,7 +29,9 @@ def main():
             "prescale": dict(collective="nccl", fuse=False),
             "symm-nccl": dict(collective="symm", flag_exchange="nccl"),
             "symm-p2p": dict(collective="symm", flag_exchange="p2p"),
-            "symm-fused": dict(collective="symm", flag_exchange="fused")}[mode]
+            "symm-fused": dict(collective="symm", flag_exchange="fused"),
+            "symm-normfirst": dict(collective="symm", flag_exchange="fused", order="norm_first"),
+            "symm-adaptive": dict(collective="symm", flag_exchange="fused", order="adaptive")}[mode]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
