@@ -62,9 +62,10 @@ def parse():
     ap.add_argument("--no-fuse", action="store_true", help="pre-scale order (K1+K2, C1, K3*1/N, SUM)")
     ap.add_argument("--collective", default="symm", choices=["symm", "nccl"],
                     help="C2 back end at N > 1: device-conditional symmetric-memory kernel or host-branch NCCL")
-    ap.add_argument("--flag-exchange", default="p2p", choices=["p2p", "fused", "nccl"],
+    ap.add_argument("--flag-exchange", default="fused", choices=["fused", "p2p", "nccl"],
                     help="fused: the whole step in one cooperative launch (symm only)")
-    ap.add_argument("--order", default="update_first", choices=["update_first", "norm_first", "adaptive"],
+    ap.add_argument("--tile", type=int, default=16384, help="elements per tile of the overlapped sync step")
+    ap.add_argument("--order", default="adaptive", choices=["update_first", "norm_first", "adaptive"],
                     help="one-launch step order (flag-exchange fused): norm_first overlaps update and mean")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -283,7 +284,7 @@ def main():
         st = SelSyncStep(w, g, cfg, momentum_buffer=mom, group=comm, fuse=not args.no_fuse,
                          collective=args.collective if world > 1 else None,
                          flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
-                         trace_capacity=1 << 14, profile=True, order=args.order)
+                         trace_capacity=1 << 14, profile=True, order=args.order, tile_elems=args.tile)
         return st
 
     def run(step, n, host_ring=None, host_row=None):

@@ -58,8 +58,9 @@ class SelSyncStep:
         broadcast_init: bool = True,
         profile: bool = False,
         timeout_s: float = 30.0,
-        order: str = "update_first",
+        order: str = "adaptive",
         order_threshold: float = 0.3,
+        tile_elems: int = 16384,
     ):
         if not isinstance(config, SelSyncConfig):
             raise ConfigError("config must be a SelSyncConfig")
@@ -79,7 +80,7 @@ class SelSyncStep:
         if collective not in ("nccl", "symm"):
             raise ConfigError(f"collective must be 'nccl' or 'symm', got {collective!r}")
         if flag_exchange is None:
-            flag_exchange = "p2p" if collective == "symm" else "nccl"
+            flag_exchange = "fused" if collective == "symm" else "nccl"
         if flag_exchange not in ("nccl", "p2p", "fused"):
             raise ConfigError(f"flag_exchange must be 'fused', 'p2p' or 'nccl', got {flag_exchange!r}")
         if collective == "symm" and config.aggregation != "params":
@@ -103,7 +104,8 @@ class SelSyncStep:
         if self.collective == "symm":
             self.symm = SymmetricParams(params.numel(), self.device, self.comm,
                                         ring_capacity=trace_capacity, timeout_s=timeout_s,
-                                        order=order, order_threshold=order_threshold)
+                                        order=order, order_threshold=order_threshold,
+                                        tile_elems=tile_elems)
             self.symm.buf.copy_(params)
             params = self.symm.buf  # the step owns the symmetric copy; use step.params
             if self.flag_exchange == "fused" and not self.symm.one_launch_capable:
