@@ -309,7 +309,7 @@ def main():
     def timed(step, n, **kw):
         comm.barrier(dev)
         torch.cuda.synchronize()
-        launches0 = K.LAUNCHES
+        launches0 = K.LAUNCHES + device_launches(step)
         k0 = len(step.kernel_events)
         s0 = len(step.sync_events)
         d0 = step.steps_done
@@ -324,7 +324,8 @@ def main():
         kms = step.kernel_ms()[k0:]
         sms = step.sync_ms()[s0:]
         dec = step.decisions()[d0 - step.steps_done:]
-        return dict(ms=ms, decisions=dec, kernel_ms=kms, sync_ms=sms, launches=K.LAUNCHES - launches0)
+        return dict(ms=ms, decisions=dec, kernel_ms=kms, sync_ms=sms,
+                    launches=K.LAUNCHES + device_launches(step) - launches0)
 
     clocks = ClockSampler(local)
     # ---- headline: 50% sync mix, device-resident inputs
@@ -523,6 +524,12 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
     if world > 1:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
+
+
+def device_launches(step) -> int:
+    """Kernels our step kernel launched from the device (CUDA dynamic parallelism)."""
+    sp = getattr(step, "symm", None)
+    return 0 if sp is None else int(sp.child_launches.item())
 
 
 def exchange_stats(m, P, world):

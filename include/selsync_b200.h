@@ -203,6 +203,7 @@ typedef struct ss_symm_group {
     float* predictor;                   /* EWMA of agreed sync decisions (zeroed) */
     int64_t tile_elems;                 /* elements per tile, multiple of 4 */
     int64_t n_tiles;                    /* capacity of every tile_cnt array */
+    uint32_t* child_launches;           /* optional: +1 per device-side (tail) launch */
 } ss_symm_group;
 
 /* bytes of each rank's signal region (flag slots + done slots, uint64 each) */

@@ -87,6 +87,7 @@ class SymmGroupC(Structure):
         ("predictor", c_void_p),
         ("tile_elems", c_int64),
         ("n_tiles", c_int64),
+        ("child_launches", c_void_p),
     ]
 
 

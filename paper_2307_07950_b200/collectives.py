@@ -179,6 +179,8 @@ class SymmetricParams:
         g.predictor = self.predictor.data_ptr()
         g.tile_elems = int(tile_elems)
         g.n_tiles = int(self.n_tiles)
+        self.child_launches = torch.zeros(1, dtype=torch.int32, device=self.device)
+        g.child_launches = self.child_launches.data_ptr()
         self.group_c = g
         self.group_ref = ctypes.byref(g)
         torch.cuda.synchronize(self.device)

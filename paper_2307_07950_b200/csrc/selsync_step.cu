@@ -54,6 +54,7 @@ struct OverlapArgs {
     int64_t n_tiles;
     int lag;                   // groups between an update ticket and the owner's mean ticket
     unsigned long long* ticket;
+    uint32_t* child_launches;  // optional launch counter (device-side launches)
 };
 
 struct Grids {
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
     if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
     const bool sync = w == SS_FLAG_SYNC;
     if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (sync ? 0.25f : 0.0f);
+    if (o.child_launches && (norm_first || sync)) atomicAdd(o.child_launches, 1u);
     if (norm_first) {
         if (sync) {
             upd_avg_kernel<MOM, NEST, W><<<gr.ua, kThreads, 0, cudaStreamTailLaunch>>>(a, s, o, seq, *o.epoch + 1);
@@ -277,6 +279,7 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
     if (rc) return rc;
     if (grp->bufs[grp->rank] != w) return fail(SS_ERR_CONFIG, "w must be this rank's symmetric buffer");
     OverlapArgs o{};
+    o.child_launches = grp->child_launches;
     o.mode = grp->order_mode;
     o.threshold = grp->order_threshold;
     if (o.mode < 0 || o.mode > 2) return fail(SS_ERR_CONFIG, "order_mode must be 0, 1 or 2, got %d", o.mode);
