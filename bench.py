@@ -340,6 +340,35 @@ def main():
         st = make_step(delta)
         run(st, max(3, args.warmup))
         modes[name] = timed(st, args.steps)
+    # ---- C2 alone (NVLink roofline of the mean): ss_symm_sync_f32 with the word forced to sync
+    c2 = None
+    if world > 1 and args.collective == "symm":
+        sp = mixed.symm
+        one = torch.ones(1, dtype=torch.int32, device=dev)
+        cs = torch.cuda.current_stream().cuda_stream
+        for _ in range(3):
+            sp.sync_(one, mixed.ws.ptr, exchange=False, stream=cs)
+        torch.cuda.synchronize()
+        comm.barrier(dev)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = max(5, min(args.steps, 50))
+        ea.record()
+        for _ in range(reps):
+            sp.sync_(one, mixed.ws.ptr, exchange=False, stream=cs)
+        eb.record()
+        torch.cuda.synchronize()
+        sp.check()
+        t = comm.max_float(ea.elapsed_time(eb), dev) / reps
+        algbw = 4 * P / (t * 1e-3) / 1e9
+        busbw = algbw * 2 * (world - 1) / world
+        c2 = {"kernel": f"ss_symm_sync_f32 ({'NVLS multimem' if sp.multicast else 'P2P two-shot'}), word forced to sync",
+              "mean_ms": t, "nvlink": {
+                  "busbw": busbw, "algbw": algbw, "unit": "GB/s", "peak_nominal": NVLINK_NOMINAL_GBS,
+                  "frac_nominal": busbw / NVLINK_NOMINAL_GBS,
+                  "ref_nccl_allreduce_busbw_1GiB_8gpu": NVLINK_ALLREDUCE_MEASURED_GBS,
+                  "frac_of_ref": busbw / NVLINK_ALLREDUCE_MEASURED_GBS},
+              "sync_step_overlap_note": ("with the adaptive order a sync step overlaps the update with this "
+                                         "mean (modes.all_sync.ms_per_step)")}
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -370,8 +399,8 @@ def main():
     kernel_name = ("ss_update_norm_signal_f32 (K13+K2: fused SGD-momentum-wd update + ||g||^2 + signal step)"
                    if not args.no_fuse else "ss_norm_signal_f32 (K1+K2)")
     if one_launch:
-        kernel_name = ("ss_step_symm_f32 (one cooperative launch: K13+K2 + P2P vote exchange + "
-                       "conditional NVLink mean; timed on local steps)")
+        kernel_name = ("ss_step_symm_f32 (one host launch: K13+K2 + P2P vote exchange; the NVLink "
+                       "mean is a device-side launch on sync steps only; timed on local steps)")
     sync_frac = sum(1 for d in res["decisions"] if d) / len(res["decisions"])
     line = {
         "metric": METRIC,
@@ -413,19 +442,8 @@ def main():
         ent.update(exchange_stats(m, P, world))
         line["modes"][name] = ent
     line.update({"exchange": exchange_stats(res, P, world)} if world > 1 else {})
-    if one_launch:
-        # the mean runs inside the step launch: its cost is the sync-minus-local launch time
-        ks = modes["all_sync"]["kernel_ms"]
-        t = sum(ks) / len(ks) - k_mean
-        if t > 0:
-            algbw = 4 * P / (t * 1e-3) / 1e9
-            busbw = algbw * 2 * (world - 1) / world
-            line["exchange"] = {"sync_mean_ms_in_launch": t, "nvlink": {
-                "busbw": busbw, "algbw": algbw, "unit": "GB/s", "peak_nominal": NVLINK_NOMINAL_GBS,
-                "frac_nominal": busbw / NVLINK_NOMINAL_GBS,
-                "ref_nccl_allreduce_busbw_1GiB_8gpu": NVLINK_ALLREDUCE_MEASURED_GBS,
-                "frac_of_ref": busbw / NVLINK_ALLREDUCE_MEASURED_GBS,
-                "how": "(sync-step launch time - local-step launch time) of ss_step_symm_f32"}}
+    if one_launch and c2 is not None:
+        line["exchange"] = c2
     if e2e is not None:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -474,7 +492,9 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
     launches = K.LAUNCHES - l0
     kms = st.kernel_ms()[k0:]
     dec = st.decisions()[d0 - st.steps_done:]
-    k_mean = sum(kms) / len(kms)
+    # roofline of the update launch on local steps (sync steps add the mean)
+    local_ms = [t for t, d in zip(kms, dec) if not d] if world > 1 else kms
+    k_mean = sum(local_ms) / len(local_ms) if local_ms else float("nan")
     nbytes = (20 if wl.momentum else 12) * st.params.numel()
     # e2e: public blocking API, batch copied from pinned host memory, loss read back
     e2e = None
@@ -513,7 +533,8 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
         "roofline": {"bound": "hbm", "kernel": "SelSync update launch (K13+K2[+exchange])",
                      "achieved": nbytes / (k_mean * 1e-3) / 1e9, "peak": hbm_peak, "peak_source": hbm_src,
                      "unit": "GB/s", "frac": nbytes / (k_mean * 1e-3) / 1e9 / hbm_peak, "traffic": None,
-                     "kernel_ms_mean": k_mean, "hot_path_share_of_step": k_mean / (ms / args.steps)},
+                     "kernel_ms_mean": k_mean, "timed_on": "local steps" if world > 1 else "all steps",
+                     "hot_path_share_of_step": sum(kms) / len(kms) / (ms / args.steps)},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
