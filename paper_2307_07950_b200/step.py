@@ -262,6 +262,14 @@ class SelSyncStep:
         s = self.signal.read_state()
         if int(s["error"]):
             K.raise_for_word(int(s["error"]) & 6 or 2, " (device signal state)")
+        if self.symm is not None and self.steps_done:
+            # a peer's NaN reaches every rank through the agreed word (MAX >= 2)
+            cap = self.symm.ring_capacity
+            ring = self.symm.agreed.cpu().numpy()
+            lo = max(0, self.steps_done - cap)
+            bad = [s for s in range(lo, self.steps_done) if int(ring[s % cap]) >= 2]
+            if bad:
+                K.raise_for_word(int(ring[bad[0] % cap]), f" (agreed flag word at step {bad[0]})")
 
     def decisions(self) -> list[bool]:
         """Agreed decision of every step still in the trace ring (True = sync)."""

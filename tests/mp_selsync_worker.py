@@ -69,5 +69,38 @@ def main():
     dist.destroy_process_group()
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "nan"):
     main()
+
+
+def nan_main():
+    """A NaN gradient on ONE rank must raise SignalError on EVERY rank (the
+    error bit travels with the agreed word), and no rank may average."""
+    out = Path(sys.argv[2])
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    from paper_2307_07950_b200 import SignalError
+
+    P = 4096
+    w = torch.zeros(P, device=dev)
+    g = torch.ones(P, device=dev)
+    step = SelSyncStep(w, g, SelSyncConfig(delta=0.1, warmup=1))
+    step.step_async(0.1)
+    if rank == 1:
+        g[7] = float("nan")
+    step.step_async(0.1)
+    raised = False
+    try:
+        step.synchronize()
+    except SignalError:
+        raised = True
+    np.savez(out / f"nan_rank{rank}.npz", raised=np.array(raised))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "nan":
+    nan_main()

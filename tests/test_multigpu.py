@@ -44,3 +44,14 @@ def test_nccl_ranks_match_reference(name, n, mode, tmp_path, golden_cases):
         np.testing.assert_allclose(z["ewma"], c["ewma"][:, rank], rtol=1e-5)
         np.testing.assert_allclose(z["delta_g"], c["delta_g"][:, rank], rtol=1e-5, atol=1e-12)
         params_close(z["params"], c["finals"][rank])
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_nan_on_one_rank_raises_everywhere(tmp_path):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29534",
+           str(ROOT / "tests" / "mp_selsync_worker.py"), "nan", str(tmp_path)]
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+    for r in range(2):
+        assert bool(np.load(tmp_path / f"nan_rank{r}.npz")["raised"])
