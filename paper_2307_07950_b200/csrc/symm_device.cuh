@@ -95,41 +95,19 @@ __device__ __forceinline__ float4 scale4(float4 v, float s) {
 template <int W>
 __device__ void average_block_range(const SymmArgs& a, int64_t e0, int64_t e1) {
     const int64_t v0 = e0 >> 2, v1 = e1 >> 2;
-    const int64_t bs = blockDim.x;
-    int64_t i = v0 + threadIdx.x;
     if constexpr (W == 0) {
-        constexpr int U = 4;  // 16-byte multimem requests in flight per thread
-        for (; i + (U - 1) * bs < v1; i += U * bs) {
-            float4 x[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) x[u] = mm_ld_reduce_add4(a.mc + 4 * (i + u * bs));
-#pragma unroll
-            for (int u = 0; u < U; ++u) mm_st4(a.mc + 4 * (i + u * bs), scale4(x[u], a.scale));
+        int64_t i = v0 + threadIdx.x;
+        for (; i + blockDim.x < v1; i += 2 * blockDim.x) {
+            float4 x = mm_ld_reduce_add4(a.mc + 4 * i);
+            float4 y = mm_ld_reduce_add4(a.mc + 4 * (i + blockDim.x));
+            mm_st4(a.mc + 4 * i, scale4(x, a.scale));
+            mm_st4(a.mc + 4 * (i + blockDim.x), scale4(y, a.scale));
         }
-        for (; i < v1; i += bs) mm_st4(a.mc + 4 * i, scale4(mm_ld_reduce_add4(a.mc + 4 * i), a.scale));
-        for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += bs)
+        for (; i < v1; i += blockDim.x) mm_st4(a.mc + 4 * i, scale4(mm_ld_reduce_add4(a.mc + 4 * i), a.scale));
+        for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x)
             mm_st1(a.mc + j, mm_ld_reduce_add1(a.mc + j) * a.scale);
     } else {
-        constexpr int U = W <= 2 ? 4 : (W <= 4 ? 2 : 1);  // peer loads in flight per thread: U * W
-        for (; i + (U - 1) * bs < v1; i += U * bs) {
-            float4 v[U][W];
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int r = 0; r < W; ++r) v[u][r] = __ldcg(reinterpret_cast<const float4*>(a.bufs[r]) + i + u * bs);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                float4 acc = v[u][0];
-#pragma unroll
-                for (int r = 1; r < W; ++r) {
-                    acc.x += v[u][r].x; acc.y += v[u][r].y; acc.z += v[u][r].z; acc.w += v[u][r].w;
-                }
-                acc = scale4(acc, a.scale);
-#pragma unroll
-                for (int r = 0; r < W; ++r) __stcg(reinterpret_cast<float4*>(a.bufs[r]) + i + u * bs, acc);
-            }
-        }
-        for (; i < v1; i += bs) {
+        for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
             float4 v[W];
 #pragma unroll
             for (int r = 0; r < W; ++r) v[r] = __ldcg(reinterpret_cast<const float4*>(a.bufs[r]) + i);
@@ -142,7 +120,7 @@ __device__ void average_block_range(const SymmArgs& a, int64_t e0, int64_t e1) {
 #pragma unroll
             for (int r = 0; r < W; ++r) __stcg(reinterpret_cast<float4*>(a.bufs[r]) + i, acc);
         }
-        for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += bs) {
+        for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x) {
             float acc = __ldcg(a.bufs[0] + j);
 #pragma unroll
             for (int r = 1; r < W; ++r) acc += __ldcg(a.bufs[r] + j);
