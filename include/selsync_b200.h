@@ -148,6 +148,22 @@ SS_API int ss_update_norm_signal_f32(float* w_dev, const float* g_dev, float* m_
                               double delta, int32_t* word_dev, ss_trace_row* trace_dev,
                               int32_t trace_cap, void* ws_dev, void* stream);
 
+/* K3 / K13+K2 over a LIST of tensors (no flat buffer): HOST arrays of device
+   pointers w[k], g[k], m[k] (m may be NULL when momentum == 0) and sizes[k].
+   Same arithmetic as ss_sgd_update_f32 / ss_update_norm_signal_f32; the norm
+   covers all tensors and finishes deterministically in one block (one logical
+   launch per <= 128 tensors). */
+SS_API int ss_sgd_update_multi_f32(float* const* w_host, const float* const* g_host, float* const* m_host,
+                                   const int64_t* sizes_host, int32_t count, float lr, float momentum,
+                                   float dampening, float weight_decay, int32_t nesterov, int32_t first_step,
+                                   const int32_t* sync_word_dev, float sync_scale, void* stream);
+SS_API int ss_update_norm_signal_multi_f32(float* const* w_host, const float* const* g_host,
+                                           float* const* m_host, const int64_t* sizes_host, int32_t count,
+                                           float lr, float momentum, float dampening, float weight_decay,
+                                           int32_t nesterov, int32_t first_step, ss_signal_state* st_dev,
+                                           double delta, int32_t* word_dev, ss_trace_row* trace_dev,
+                                           int32_t trace_cap, void* ws_dev, void* stream);
+
 /* ---------------- simulated workers on one device ---------------- */
 
 /* aggregate_mean (strategies.py:159-168) over `count` replica buffers in

@@ -15,7 +15,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRCS = [PKG / "csrc" / f for f in ("selsync_b200.cu", "selsync_symm.cu", "selsync_step.cu")]
+SRCS = [PKG / "csrc" / f for f in ("selsync_b200.cu", "selsync_symm.cu", "selsync_step.cu", "selsync_multi.cu")]
 DEPS = [*SRCS, *sorted((PKG / "csrc").glob("*.cuh"))]
 HEADER = ROOT / "include" / "selsync_b200.h"
 OUT = PKG / "_lib" / "libselsync_b200.so"

@@ -121,6 +121,16 @@ _SIGS = {
          _P, c_double, _P, _P, c_int32, _P, _P],
         c_int,
     ),
+    "ss_sgd_update_multi_f32": (
+        [POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), POINTER(c_int64), c_int32, c_float, c_float,
+         c_float, c_float, c_int32, c_int32, _P, c_float, _P],
+        c_int,
+    ),
+    "ss_update_norm_signal_multi_f32": (
+        [POINTER(c_void_p), POINTER(c_void_p), POINTER(c_void_p), POINTER(c_int64), c_int32, c_float, c_float,
+         c_float, c_float, c_int32, c_int32, _P, c_double, _P, _P, c_int32, _P, _P],
+        c_int,
+    ),
     "ss_replica_average_f32": ([POINTER(c_void_p), c_int32, c_int64, _P], c_int),
     "ss_replica_sum_f32": ([POINTER(c_void_p), c_int32, c_int64, _P], c_int),
     "ss_mean_f32": ([POINTER(c_void_p), c_int32, c_int64, _P, _P], c_int),

@@ -278,3 +278,47 @@ def step_symm_(w, g, m, signal: DeviceSignal, ws: Workspace, group, *, lr: float
         int(bool(first_step)), signal.state.data_ptr(), float(delta), signal.word.data_ptr(),
         signal.trace.data_ptr(), signal.trace_capacity, group.group_ref, ws.ptr, stream_of(w)))
     _count()
+
+
+def _tensor_table(ws, gs, ms, momentum):
+    if not ws or len(ws) != len(gs) or (momentum != 0.0 and (ms is None or len(ms) != len(ws))):
+        raise ConfigError("parameter / gradient / momentum lists must have equal lengths")
+    dev = ws[0].device
+    for i, (w, g) in enumerate(zip(ws, gs)):
+        _need(w, torch.float32, f"params[{i}]", dev)
+        _need(g, torch.float32, f"grads[{i}]", dev)
+        if g.numel() != w.numel():
+            raise ConfigError(f"gradient {i} does not match its parameter")
+        if momentum != 0.0:
+            _need(ms[i], torch.float32, f"momentum[{i}]", dev)
+            if ms[i].numel() != w.numel():
+                raise ConfigError(f"momentum buffer {i} does not match its parameter")
+    wp = N.ptr_array([w.data_ptr() for w in ws])
+    gp = N.ptr_array([g.data_ptr() for g in gs])
+    mp = N.ptr_array([m.data_ptr() for m in ms]) if momentum != 0.0 else N.ptr_array([0] * len(ws))
+    sizes = (ctypes.c_int64 * len(ws))(*[w.numel() for w in ws])
+    return wp, gp, mp, sizes
+
+
+def sgd_update_multi_(ws, gs, ms=None, *, lr: float, momentum: float = 0.0, dampening: float = 0.0,
+                      weight_decay: float = 0.0, nesterov: bool = False, first_step: bool = False,
+                      sync_word: Optional[torch.Tensor] = None, sync_scale: float = 1.0) -> None:
+    """K3 over a tensor list (pointer table)."""
+    wp, gp, mp, sizes = _tensor_table(ws, gs, ms, momentum)
+    N.check(N.LIB.ss_sgd_update_multi_f32(
+        wp, gp, mp, sizes, len(ws), float(lr), float(momentum), float(dampening), float(weight_decay),
+        int(bool(nesterov)), int(bool(first_step)), _ptr(sync_word), float(sync_scale), stream_of(ws[0])))
+    _count((len(ws) + 127) // 128)
+
+
+def update_norm_signal_multi_(ws, gs, ms, signal: DeviceSignal, workspace: Workspace, *, lr: float,
+                              delta: float, momentum: float = 0.0, dampening: float = 0.0,
+                              weight_decay: float = 0.0, nesterov: bool = False, first_step: bool = False) -> None:
+    """K13 + K2 over a tensor list: one pass, ||g||^2 over all tensors, the vote."""
+    wp, gp, mp, sizes = _tensor_table(ws, gs, ms, momentum)
+    N.check(N.LIB.ss_update_norm_signal_multi_f32(
+        wp, gp, mp, sizes, len(ws), float(lr), float(momentum), float(dampening), float(weight_decay),
+        int(bool(nesterov)), int(bool(first_step)), signal.state.data_ptr(), float(delta),
+        signal.word.data_ptr(), signal.trace.data_ptr(), signal.trace_capacity, workspace.ptr,
+        stream_of(ws[0])))
+    _count((len(ws) + 127) // 128)

@@ -324,3 +324,80 @@ class SelSyncStep:
 
     def sync_ms(self) -> list[float]:
         return [a.elapsed_time(b) for a, b in self.sync_events]
+
+
+class TensorListSelSyncStep:
+    """SelSync step over a LIST of parameter / gradient tensors (no flat
+    buffer): K13+K2 over a pointer table (``ss_update_norm_signal_multi_f32``,
+    ||g||^2 of the whole model in one logical launch), C1 as an NCCL
+    allreduce-MAX of the flag word, and on sync steps the parameter mean as
+    NCCL allreduce-AVG over the tensors, coalesced into one NCCL group.
+
+    Use it when the model's storage cannot be re-pointed at flat buffers;
+    ``SelSyncStep`` over ``FlatParameters`` is the faster path.
+    """
+
+    def __init__(self, params, grads, config: SelSyncConfig, *, momentum_buffers=None, group=None,
+                 trace_capacity: int = 4096, broadcast_init: bool = True):
+        if not isinstance(config, SelSyncConfig):
+            raise ConfigError("config must be a SelSyncConfig")
+        if config.aggregation != "params":
+            raise ConfigError("TensorListSelSyncStep implements parameter aggregation")
+        self.params, self.grads = list(params), list(grads)
+        if not self.params or len(self.params) != len(self.grads):
+            raise ConfigError("params and grads must be non-empty lists of equal length")
+        self.config = config
+        self.device = self.params[0].device
+        if config.momentum != 0.0 and momentum_buffers is None:
+            momentum_buffers = [torch.zeros_like(p) for p in self.params]
+        self.momentum = list(momentum_buffers) if config.momentum != 0.0 else None
+        self.comm = group if isinstance(group, RankGroup) else RankGroup(group)
+        self.world = self.comm.size
+        self.signal = K.DeviceSignal(self.device, config.smoothing_for(self.world), config.warmup,
+                                     trace_capacity)
+        self.ws = K.Workspace(self.device)
+        self._word_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._ready = torch.cuda.Event()
+        self.steps_done = 0
+        self.decision_log: list[bool] = []
+        if broadcast_init and self.world > 1:
+            for p in self.params:
+                self.comm.broadcast_(p, 0)
+
+    def _average(self) -> None:
+        import torch.distributed as dist
+
+        try:
+            from torch.distributed.distributed_c10d import _coalescing_manager
+        except ImportError:  # pragma: no cover - older torch
+            _coalescing_manager = None
+        if _coalescing_manager is not None and self.comm.backend == "nccl":
+            with _coalescing_manager(group=self.comm.group, device=self.device):
+                for p in self.params:
+                    dist.all_reduce(p, op=dist.ReduceOp.AVG, group=self.comm.group)
+        else:
+            for p in self.params:
+                self.comm.average_(p)
+
+    def step(self, lr: float) -> str:
+        lr = float(lr)
+        if not (lr >= 0.0) or not math.isfinite(lr):
+            raise ConfigError(f"learning rate must be non-negative, got {lr}")
+        c = self.config
+        K.update_norm_signal_multi_(self.params, self.grads, self.momentum, self.signal, self.ws, lr=lr,
+                                    delta=c.delta, momentum=c.momentum, dampening=c.dampening,
+                                    weight_decay=c.weight_decay, nesterov=c.nesterov,
+                                    first_step=self.steps_done == 0)
+        self.comm.agree(self.signal.word)
+        self._word_host.copy_(self.signal.word, non_blocking=True)
+        self._ready.record(torch.cuda.current_stream(self.device))
+        self._ready.synchronize()
+        word = int(self._word_host[0])
+        if word >= 2:
+            K.raise_for_word(word, f" (agreed flag word {word} at step {self.steps_done})")
+        synced = bool(word & 1)
+        if synced and self.world > 1:
+            self._average()
+        self.steps_done += 1
+        self.decision_log.append(synced)
+        return "sync" if synced else "local"
