@@ -14,12 +14,17 @@ Device work per step, parameter aggregation (the default):
           -- NCCL (default) or the P2P exchange inside the C2 kernel
   C2      sync steps only: the parameter mean (runtime.py:275-294)
 
-Two C2 back ends:
-  collective="symm" (default when world > 1): parameters live in symmetric
-      memory and ``ss_symm_sync_f32`` reads the agreed word ON THE DEVICE and
-      averages only when it says sync (NVLS multimem reduce + broadcast, 1/N
-      in the epilogue). No host round-trip: ``step_async`` enqueues a whole
-      step and returns immediately; the host reads decisions lazily.
+Back ends (N > 1):
+  collective="symm" (default): parameters live in symmetric memory.
+      flag_exchange="fused" (default): the whole step is ONE host launch
+      (``ss_step_symm_f32``): update + norm + vote, the vote exchange over
+      NVLink in the last block, and on sync a device-side launch of the mean
+      (NVLS multimem or P2P, 1/N in the epilogue); ``order`` picks update-first,
+      norm-first (update and mean overlapped tile by tile) or adaptive.
+      flag_exchange="p2p" / "nccl": K13, then ``ss_symm_sync_f32`` reading the
+      agreed word (its own P2P exchange, or an NCCL allreduce-MAX before it).
+      No host round-trip in any of them: ``step_async`` enqueues a whole step
+      and returns; the host reads decisions lazily.
   collective="nccl": the host reads the agreed word (4-byte pinned copy) and
       issues NCCL allreduce-AVG on sync steps. ``fuse=False`` selects the
       pre-scale order instead: K1+K2, C1, K3 whose epilogue multiplies by 1/N
