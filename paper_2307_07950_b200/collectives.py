@@ -192,6 +192,14 @@ class SymmetricParams:
         N.check(N.LIB.ss_symm_sync_f32(self.group_ref, self.buf.numel(), word.data_ptr(), int(exchange),
                                        1.0 / self.world, ws_ptr, stream))
 
+    def enable_timeline(self, capacity: int) -> torch.Tensor:
+        """Record the per-ticket timeline of the overlapped sync step (tooling):
+        4 x int64 per ticket {kind << 48 | tile, t_start, t_ready, t_end} (ns)."""
+        self.timeline = torch.zeros(4 * int(capacity), dtype=torch.int64, device=self.device)
+        self.group_c.debug_events = self.timeline.data_ptr()
+        self.group_c.debug_cap = int(capacity)
+        return self.timeline
+
     @property
     def one_launch_capable(self) -> bool:
         """The fused one-launch step supports NVLS or P2P widths 2, 4, 8."""

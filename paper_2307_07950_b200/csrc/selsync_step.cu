@@ -55,6 +55,8 @@ struct OverlapArgs {
     int lag;                   // groups between an update ticket and the owner's mean ticket
     unsigned long long* ticket;
     uint32_t* child_launches;  // optional launch counter (device-side launches)
+    uint64_t* dbg;             // optional per-ticket timeline: {kind << 48 | tile, t0, t_ready, t_end}
+    int64_t dbg_cap;
 };
 
 struct Grids {
@@ -114,9 +116,13 @@ __global__ void __launch_bounds__(kThreads, 4) upd_avg_kernel(SgdArgs a, SymmArg
         if (k >= total) break;
         const int64_t grp = static_cast<int64_t>(k / (N + 1));
         const int pos = static_cast<int>(k % (N + 1));
+        const bool rec = o.dbg != nullptr && static_cast<int64_t>(k) < o.dbg_cap && threadIdx.x == 0;
+        uint64_t t_start = rec ? now_ns() : 0, t_ready = 0;
+        int64_t rec_tile = -1;
         if (pos < N) {
             const int64_t t = grp * N + pos;  // update tile t (owner t % N)
             if (t < o.n_tiles) {
+                rec_tile = t;
                 const int64_t e0 = t * o.tile;
                 const int64_t e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
                 sgd_block_range<MOM, NEST>(a, e0, e1);
@@ -130,6 +136,7 @@ __global__ void __launch_bounds__(kThreads, 4) upd_avg_kernel(SgdArgs a, SymmArg
             const int64_t m = grp - o.lag;
             const int64_t t = m * N + s.rank;  // mean of owned tile t once all N ranks updated it
             if (m >= 0 && t < o.n_tiles) {
+                rec_tile = t;
                 if (threadIdx.x == 0) {
                     const uint64_t t0 = now_ns();
                     while (static_cast<int32_t>(ld_acquire_sys_u32(o.cnt[s.rank] + t) - target) < 0) {
@@ -141,10 +148,19 @@ __global__ void __launch_bounds__(kThreads, 4) upd_avg_kernel(SgdArgs a, SymmArg
                     }
                 }
                 __syncthreads();
+                if (rec) t_ready = now_ns();
                 const int64_t e0 = t * o.tile;
                 const int64_t e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
                 average_block_range<W>(s, e0, e1);
             }
+        }
+        if (rec && rec_tile >= 0) {
+            __threadfence_block();
+            uint64_t* e = o.dbg + 4 * k;
+            e[0] = (static_cast<uint64_t>(pos < N ? 0 : 1) << 48) | static_cast<uint64_t>(rec_tile);
+            e[1] = t_start;
+            e[2] = t_ready ? t_ready : t_start;
+            e[3] = now_ns();
         }
     }
     __threadfence_system();
@@ -280,6 +296,8 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
     if (grp->bufs[grp->rank] != w) return fail(SS_ERR_CONFIG, "w must be this rank's symmetric buffer");
     OverlapArgs o{};
     o.child_launches = grp->child_launches;
+    o.dbg = grp->debug_events;
+    o.dbg_cap = grp->debug_events ? grp->debug_cap : 0;
     o.mode = grp->order_mode;
     o.threshold = grp->order_threshold;
     if (o.mode < 0 || o.mode > 2) return fail(SS_ERR_CONFIG, "order_mode must be 0, 1 or 2, got %d", o.mode);

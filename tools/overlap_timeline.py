@@ -1,0 +1,70 @@
+"""Timeline of the overlapped (norm-first) sync step: per-ticket timestamps
+from the device, summarised per rank (torchrun, one rank per GPU)."""
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2307_07950_b200 import SelSyncConfig  # noqa: E402
+from paper_2307_07950_b200.step import SelSyncStep  # noqa: E402
+
+P = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+tile = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+local = int(os.environ["LOCAL_RANK"])
+torch.cuda.set_device(local)
+dev = torch.device("cuda", local)
+dist.init_process_group("nccl", device_id=dev)
+w = torch.randn(P, device=dev)
+g = torch.randn(P, device=dev)
+cfg = SelSyncConfig(delta=0.0, warmup=1, momentum=0.9, weight_decay=4e-4)
+st = SelSyncStep(w, g, cfg, order="norm_first", tile_elems=tile)
+for _ in range(5):
+    st.step_async(0.01)
+st.synchronize()
+cap = 8 * (P // tile + 64)
+tl = st.symm.enable_timeline(cap)
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+st.step_async(0.01)
+b.record()
+st.synchronize()
+ms = a.elapsed_time(b)
+ev = tl.view(-1, 4).cpu().numpy()
+ev = ev[ev[:, 1] > 0]
+kind = ev[:, 0] >> 48
+t0 = ev[:, 1].min()
+out = {}
+for name, kk in (("update", 0), ("mean", 1)):
+    e = ev[kind == kk]
+    if len(e) == 0:
+        continue
+    wait = (e[:, 2] - e[:, 1]) / 1e3
+    run = (e[:, 3] - e[:, 2]) / 1e3
+    out[name] = (len(e), wait.mean(), run.mean(), (e[:, 1].min() - t0) / 1e3, (e[:, 3].max() - t0) / 1e3,
+                 np.percentile(run, 90))
+span = (ev[:, 3].max() - t0) / 1e3
+lines = [f"rank {rank}: step {ms*1e3:.0f} us (events), overlapped kernel span {span:.0f} us"]
+for name, (n, wt, rn, first, last, p90) in out.items():
+    lines.append(f"   {name:6s} tasks {n:5d}  wait {wt:7.1f} us  run {rn:7.1f} us (p90 {p90:.1f})  "
+                 f"first start {first:7.0f} us  last end {last:7.0f} us")
+# concurrency: how many mean tasks were running over time
+m = ev[kind == 1]
+if len(m):
+    grid = np.linspace(0, span, 20)
+    conc = [int(((m[:, 2] - t0) / 1e3 <= x).sum() - ((m[:, 3] - t0) / 1e3 <= x).sum()) for x in grid]
+    upd = ev[kind == 0]
+    concu = [int(((upd[:, 1] - t0) / 1e3 <= x).sum() - ((upd[:, 3] - t0) / 1e3 <= x).sum()) for x in grid]
+    lines.append("   running mean tasks over time:   " + " ".join(f"{c:3d}" for c in conc))
+    lines.append("   running update tasks over time: " + " ".join(f"{c:3d}" for c in concu))
+txt = "\n".join(lines)
+all_txt = [None] * world
+dist.all_gather_object(all_txt, txt)
+if rank == 0:
+    print("\n".join(all_txt), flush=True)
+dist.barrier(device_ids=[local])
+dist.destroy_process_group()
