@@ -371,11 +371,37 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
 // The update over elements [e0, e1) by the threads of ONE block (tile work of
 // the overlapped sync step). Requires 16-byte-aligned streams (head == 0) and
 // e0 % 4 == 0; a scalar tail is handled when e1 is not a multiple of 4.
-template <bool MOM, bool NEST>
+template <bool MOM, bool NEST, int U = 2>
 __device__ __forceinline__ void sgd_block_range(const SgdArgs& a, int64_t e0, int64_t e1) {
+    // U vectors per stream in flight per thread: in the overlapped step only
+    // part of the grid updates at a time, so each block needs more bytes in
+    // flight than in the whole-grid K13 sweep (where U = 1 is best)
     const float s = 1.0f;
     const int64_t v0 = e0 >> 2, v1 = e1 >> 2;
-    for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+    const int64_t bs = blockDim.x;
+    int64_t i = v0 + threadIdx.x;
+    for (; i + (U - 1) * bs < v1; i += U * bs) {
+        float4 gv[U], wv[U], mv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = 4 * (i + u * bs);
+            gv[u] = ld_cs4(a.g + k);
+            wv[u] = ld_cs4(a.w + k);
+            if (MOM) mv[u] = ld_cs4(a.m + k);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = 4 * (i + u * bs);
+            float4 mm = MOM ? mv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
+            sgd_elem<MOM, NEST>(wv[u].x, gv[u].x, mm.x, a, s);
+            sgd_elem<MOM, NEST>(wv[u].y, gv[u].y, mm.y, a, s);
+            sgd_elem<MOM, NEST>(wv[u].z, gv[u].z, mm.z, a, s);
+            sgd_elem<MOM, NEST>(wv[u].w, gv[u].w, mm.w, a, s);
+            st_cs4(a.w + k, wv[u]);
+            if (MOM) st_cs4(a.m + k, mm);
+        }
+    }
+    for (; i < v1; i += bs) {
         const int64_t k = 4 * i;
         float4 gv = ld_cs4(a.g + k), wv = ld_cs4(a.w + k);
         float4 mm = MOM ? ld_cs4(a.m + k) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -387,7 +413,7 @@ __device__ __forceinline__ void sgd_block_range(const SgdArgs& a, int64_t e0, in
         if (MOM) st_cs4(a.m + k, mm);
     }
     float mdummy = 0.0f;
-    for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x) {
+    for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += bs) {
         float w = a.w[j], g = a.g[j];
         float m = MOM ? a.m[j] : 0.0f;
         sgd_elem<MOM, NEST>(w, g, MOM ? m : mdummy, a, s);

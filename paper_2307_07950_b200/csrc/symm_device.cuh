@@ -107,7 +107,28 @@ __device__ void average_block_range(const SymmArgs& a, int64_t e0, int64_t e1) {
         for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x)
             mm_st1(a.mc + j, mm_ld_reduce_add1(a.mc + j) * a.scale);
     } else {
-        for (int64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+        constexpr int U = W <= 4 ? 2 : 1;  // peer loads in flight per thread: U * W
+        const int64_t bs = blockDim.x;
+        int64_t i = v0 + threadIdx.x;
+        for (; i + (U - 1) * bs < v1; i += U * bs) {
+            float4 v[U][W];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int r = 0; r < W; ++r) v[u][r] = __ldcg(reinterpret_cast<const float4*>(a.bufs[r]) + i + u * bs);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                float4 acc = v[u][0];
+#pragma unroll
+                for (int r = 1; r < W; ++r) {
+                    acc.x += v[u][r].x; acc.y += v[u][r].y; acc.z += v[u][r].z; acc.w += v[u][r].w;
+                }
+                acc = scale4(acc, a.scale);
+#pragma unroll
+                for (int r = 0; r < W; ++r) __stcg(reinterpret_cast<float4*>(a.bufs[r]) + i + u * bs, acc);
+            }
+        }
+        for (; i < v1; i += bs) {
             float4 v[W];
 #pragma unroll
             for (int r = 0; r < W; ++r) v[r] = __ldcg(reinterpret_cast<const float4*>(a.bufs[r]) + i);
@@ -120,7 +141,7 @@ __device__ void average_block_range(const SymmArgs& a, int64_t e0, int64_t e1) {
 #pragma unroll
             for (int r = 0; r < W; ++r) __stcg(reinterpret_cast<float4*>(a.bufs[r]) + i, acc);
         }
-        for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x) {
+        for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += bs) {
             float acc = __ldcg(a.bufs[0] + j);
 #pragma unroll
             for (int r = 1; r < W; ++r) acc += __ldcg(a.bufs[r] + j);
