@@ -195,7 +195,8 @@ class SymmetricParams:
     def enable_timeline(self, capacity: int) -> torch.Tensor:
         """Record the per-ticket timeline of the overlapped sync step (tooling):
         4 x int64 per ticket {kind << 48 | tile, t_start, t_ready, t_end} (ns)."""
-        self.timeline = torch.zeros(4 * int(capacity), dtype=torch.int64, device=self.device)
+        # + 8 markers: step start, last arrival, votes in, child launched, last arrival, barrier done
+        self.timeline = torch.zeros(4 * int(capacity) + 8, dtype=torch.int64, device=self.device)
         self.group_c.debug_events = self.timeline.data_ptr()
         self.group_c.debug_cap = int(capacity)
         return self.timeline

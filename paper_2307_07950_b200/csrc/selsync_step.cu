@@ -166,7 +166,9 @@ __global__ void __launch_bounds__(kThreads, 4) upd_avg_kernel(SgdArgs a, SymmArg
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+        if (o.dbg) o.dbg[4 * o.dbg_cap + 4] = now_ns();
         end_barrier(s, seq);
+        if (o.dbg) o.dbg[4 * o.dbg_cap + 5] = now_ns();
         *o.ticket = 0ull;
         *o.epoch = epoch;
         *s.arrive = 0u;
@@ -180,6 +182,8 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
     __shared__ bool s_last;
     // the order of this step: identical on every rank (same decision history)
     const bool norm_first = o.mode == 1 || (o.mode == 2 && *reinterpret_cast<volatile float*>(o.predictor) >= o.threshold);
+    uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {step start, last arrival, votes in, child launched, end}
+    if (mark && blockIdx.x == 0 && threadIdx.x == 0) mark[0] = now_ns();
     const double acc = norm_first ? norm_pass<4>(a.g, a.n, a.head)
                                   : sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
     Workspace ws = ws_view(f.ws);
@@ -196,6 +200,7 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
     for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
     v = block_sum(v);
     if (threadIdx.x != 0) return;
+    if (mark) mark[1] = now_ns();
     *ws.counter = 0u;
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
@@ -214,10 +219,12 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
         w = -1;
     }
     *f.word = w;
+    if (mark) mark[2] = now_ns();
     if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
     const bool sync = w == SS_FLAG_SYNC;
     if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (sync ? 0.25f : 0.0f);
     if (o.child_launches && (norm_first || sync)) atomicAdd(o.child_launches, 1u);
+    if (mark) mark[3] = now_ns();
     if (norm_first) {
         if (sync) {
             upd_avg_kernel<MOM, NEST, W><<<gr.ua, kThreads, 0, cudaStreamTailLaunch>>>(a, s, o, seq, *o.epoch + 1);

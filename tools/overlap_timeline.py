@@ -34,7 +34,9 @@ st.step_async(0.01)
 b.record()
 st.synchronize()
 ms = a.elapsed_time(b)
-ev = tl.view(-1, 4).cpu().numpy()
+raw = tl.cpu().numpy()
+marks = raw[4 * cap:]
+ev = raw[: 4 * cap].reshape(-1, 4)
 ev = ev[ev[:, 1] > 0]
 kind = ev[:, 0] >> 48
 t0 = ev[:, 1].min()
@@ -48,7 +50,12 @@ for name, kk in (("update", 0), ("mean", 1)):
     out[name] = (len(e), wait.mean(), run.mean(), (e[:, 1].min() - t0) / 1e3, (e[:, 3].max() - t0) / 1e3,
                  np.percentile(run, 90))
 span = (ev[:, 3].max() - t0) / 1e3
-lines = [f"rank {rank}: step {ms*1e3:.0f} us (events), overlapped kernel span {span:.0f} us"]
+m0 = marks[0]
+lines = [f"rank {rank}: step {ms*1e3:.0f} us (events), overlapped kernel span {span:.0f} us",
+         "   step kernel: last block arrives {:.0f} us, votes in {:.0f}, child launched {:.0f}; "
+         "child first ticket {:.0f}; last arrival {:.0f}; end barrier done {:.0f} us".format(
+             (marks[1] - m0) / 1e3, (marks[2] - m0) / 1e3, (marks[3] - m0) / 1e3, (t0 - m0) / 1e3,
+             (marks[4] - m0) / 1e3, (marks[5] - m0) / 1e3)]
 for name, (n, wt, rn, first, last, p90) in out.items():
     lines.append(f"   {name:6s} tasks {n:5d}  wait {wt:7.1f} us  run {rn:7.1f} us (p90 {p90:.1f})  "
                  f"first start {first:7.0f} us  last end {last:7.0f} us")
