@@ -15,14 +15,16 @@
 //     this rank's shard with the 1/N in the epilogue (C2) + end barrier.
 //     20P HBM bytes; a sync step pays update + mean back to back.
 //
-//  norm first (order 1): K1 -- ||g||^2 only (4P); vote exchange as above;
-//     then on a local step the plain update (20P) and on a sync step
-//     upd_avg_kernel, which OVERLAPS the HBM-bound update with the
-//     NVLink-bound mean tile by tile: blocks pull tickets in a fixed order
-//     (N update tiles, then the mean of one tile this rank owns that was
-//     updated `lag` groups earlier); a rank announces a finished tile by a
-//     remote atomic add on the owner's counter, the owner reduces the tile
-//     once all N counts are in. A sync step then costs ~max(update, mean).
+//  norm first (order 1): ONE ticketed pass of the same launch, no device-side
+//     launch: first the ||g||^2 tiles (4P; the block that finishes the last
+//     one runs K2 and posts the vote), then groups of N update tiles and one
+//     mean ticket for a tile this rank owns (tile t belongs to rank t mod N)
+//     that was updated `lag` groups earlier. A rank announces a finished
+//     update tile by a remote atomic add on the owner's counter; a mean ticket
+//     waits for the agreed vote (a no-op on local steps) and for all N counts.
+//     Updates start while the vote is still in flight, and on sync steps the
+//     HBM-bound update overlaps the NVLink-bound mean tile by tile. Tickets
+//     only wait on earlier tickets, so the pass cannot deadlock.
 //
 //  adaptive (order 2): the last block keeps an EWMA of the agreed decisions;
 //     the next step uses order 1 while it is >= threshold. Both orders
@@ -57,6 +59,8 @@ struct OverlapArgs {
     uint32_t* child_launches;  // optional launch counter (device-side launches)
     uint64_t* dbg;             // optional per-ticket timeline: {kind << 48 | tile, t0, t_ready, t_end}
     int64_t dbg_cap;
+    double* tile_norm;         // fp64 ||g_tile||^2 per tile (norm-first order)
+    unsigned int* norm_done;   // finished norm tiles (self-resetting)
 };
 
 struct Grids {
@@ -95,69 +99,124 @@ __global__ void __launch_bounds__(512, 2) avg_kernel(SymmArgs s, uint64_t seq) {
     }
 }
 
-template <bool MOM, bool NEST>
-__global__ void __launch_bounds__(kThreads, 4) update_kernel(SgdArgs a) {
-    sgd_pass<MOM, NEST, false, (MOM ? 1 : 2)>(a);
+// agreed word of step `seq` from the N seq-tagged votes in this rank's signal slots
+__device__ int agreed_vote(const SymmArgs& s, uint64_t seq) {
+    bool to = false;
+    int w = 0;
+    for (int j = 0; j < s.world && !to; ++j) {
+        const uint64_t t = wait_tag(s.pads[s.rank] + j, seq, 32, s, &to);
+        const int wj = static_cast<int>(static_cast<uint32_t>(t));
+        w = wj > w ? wj : w;
+    }
+    if (to) {
+        atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+        return -1;
+    }
+    return w;
 }
 
 template <bool MOM, bool NEST, int W>
-__global__ void __launch_bounds__(kThreads, 4) upd_avg_kernel(SgdArgs a, SymmArgs s, OverlapArgs o,
-                                                               uint64_t seq, uint32_t epoch) {
+__device__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o, uint64_t seq) {
     __shared__ unsigned long long s_ticket;
+    __shared__ int s_vote;
+    __shared__ bool s_last_norm;
     const int N = s.world;
-    const int64_t groups = (o.n_tiles + N - 1) / N + o.lag;
-    const unsigned long long total = static_cast<unsigned long long>(groups) * (N + 1);
+    const int64_t T = o.n_tiles;
+    const int64_t groups = (T + N - 1) / N + o.lag;
+    const unsigned long long total = static_cast<unsigned long long>(T) + static_cast<unsigned long long>(groups) * (N + 1);
+    const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(o.epoch) + 1;
     const uint32_t target = static_cast<uint32_t>(N) * epoch;
+    if (threadIdx.x == 0) s_vote = -2;
+    __syncthreads();
     for (;;) {
         if (threadIdx.x == 0) s_ticket = atomicAdd(o.ticket, 1ull);
         __syncthreads();
         const unsigned long long k = s_ticket;
         __syncthreads();
         if (k >= total) break;
-        const int64_t grp = static_cast<int64_t>(k / (N + 1));
-        const int pos = static_cast<int>(k % (N + 1));
         const bool rec = o.dbg != nullptr && static_cast<int64_t>(k) < o.dbg_cap && threadIdx.x == 0;
         uint64_t t_start = rec ? now_ns() : 0, t_ready = 0;
         int64_t rec_tile = -1;
-        if (pos < N) {
-            const int64_t t = grp * N + pos;  // update tile t (owner t % N)
-            if (t < o.n_tiles) {
-                rec_tile = t;
-                const int64_t e0 = t * o.tile;
-                const int64_t e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
-                sgd_block_range<MOM, NEST>(a, e0, e1);
-                __syncthreads();
+        int kind = 0;
+        if (k < static_cast<unsigned long long>(T)) {
+            // ---- norm tile k of the gradient
+            const int64_t t = static_cast<int64_t>(k);
+            const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
+            double acc = 0.0;
+            for (int64_t i = (e0 >> 2) + threadIdx.x; i < (e1 >> 2); i += blockDim.x) acc = sq4(ld_cs4(a.g + 4 * i), acc);
+            for (int64_t j = 4 * (e1 >> 2) + threadIdx.x; j < e1; j += blockDim.x)
+                acc = fma((double)a.g[j], (double)a.g[j], acc);
+            const double bsum = block_sum(acc);
+            if (threadIdx.x == 0) {
+                o.tile_norm[t] = bsum;
+                __threadfence();
+                s_last_norm = atomicAdd(o.norm_done, 1u) == static_cast<unsigned int>(T - 1);
+            }
+            __syncthreads();
+            if (s_last_norm) {  // every tile's partial is in: total in a fixed order, K2, vote
+                __threadfence();
+                double v = 0.0;
+                for (int64_t i = threadIdx.x; i < T; i += blockDim.x) v += __ldcg(o.tile_norm + i);
+                v = block_sum(v);
                 if (threadIdx.x == 0) {
+                    *o.norm_done = 0u;
+                    signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+                    const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
                     __threadfence_system();
-                    red_add_release_sys(o.cnt[t % N] + t, 1u);
+                    for (int j = 0; j < N; ++j) st_release_sys(s.pads[j] + s.rank, tagged);
+                    if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
                 }
             }
+            kind = 2;
+            rec_tile = t;
         } else {
-            const int64_t m = grp - o.lag;
-            const int64_t t = m * N + s.rank;  // mean of owned tile t once all N ranks updated it
-            if (m >= 0 && t < o.n_tiles) {
-                rec_tile = t;
-                if (threadIdx.x == 0) {
-                    const uint64_t t0 = now_ns();
-                    while (static_cast<int32_t>(ld_acquire_sys_u32(o.cnt[s.rank] + t) - target) < 0) {
-                        if (now_ns() - t0 > s.timeout_ns) {
-                            atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
-                            break;
+            const unsigned long long k2 = k - static_cast<unsigned long long>(T);
+            const int64_t grp = static_cast<int64_t>(k2 / (N + 1));
+            const int pos = static_cast<int>(k2 % (N + 1));
+            if (pos < N) {
+                // ---- update tile t (owner t % N), announced to the owner
+                const int64_t t = grp * N + pos;
+                if (t < T) {
+                    const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
+                    sgd_block_range<MOM, NEST>(a, e0, e1);
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        __threadfence_system();
+                        red_add_release_sys(o.cnt[t % N] + t, 1u);
+                    }
+                    rec_tile = t;
+                }
+            } else {
+                // ---- mean of owned tile t: needs the agreed vote and all N updates
+                const int64_t m = grp - o.lag;
+                const int64_t t = m * N + s.rank;
+                if (m >= 0 && t < T) {
+                    if (threadIdx.x == 0 && s_vote == -2) s_vote = agreed_vote(s, seq);
+                    __syncthreads();
+                    if (s_vote == SS_FLAG_SYNC) {
+                        if (threadIdx.x == 0) {
+                            const uint64_t t0 = now_ns();
+                            while (static_cast<int32_t>(ld_acquire_sys_u32(o.cnt[s.rank] + t) - target) < 0) {
+                                if (now_ns() - t0 > s.timeout_ns) {
+                                    atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+                                    break;
+                                }
+                                __nanosleep(128);
+                            }
                         }
-                        __nanosleep(128);
+                        __syncthreads();
+                        if (rec) t_ready = now_ns();
+                        const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
+                        average_block_range<W>(s, e0, e1);
+                        rec_tile = t;
+                        kind = 1;
                     }
                 }
-                __syncthreads();
-                if (rec) t_ready = now_ns();
-                const int64_t e0 = t * o.tile;
-                const int64_t e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
-                average_block_range<W>(s, e0, e1);
             }
         }
         if (rec && rec_tile >= 0) {
-            __threadfence_block();
             uint64_t* e = o.dbg + 4 * k;
-            e[0] = (static_cast<uint64_t>(pos < N ? 0 : 1) << 48) | static_cast<uint64_t>(rec_tile);
+            e[0] = (static_cast<uint64_t>(kind) << 48) | static_cast<uint64_t>(rec_tile);
             e[1] = t_start;
             e[2] = t_ready ? t_ready : t_start;
             e[3] = now_ns();
@@ -166,8 +225,12 @@ __global__ void __launch_bounds__(kThreads, 4) upd_avg_kernel(SgdArgs a, SymmArg
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+        const int w = s_vote != -2 ? s_vote : agreed_vote(s, seq);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 4] = now_ns();
-        end_barrier(s, seq);
+        *f.word = w;
+        if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
+        if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (w == SS_FLAG_SYNC ? 0.25f : 0.0f);
+        if (w == SS_FLAG_SYNC) end_barrier(s, seq);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 5] = now_ns();
         *o.ticket = 0ull;
         *o.epoch = epoch;
@@ -180,12 +243,17 @@ template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o,
                                                             Grids gr) {
     __shared__ bool s_last;
+    const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     // the order of this step: identical on every rank (same decision history)
     const bool norm_first = o.mode == 1 || (o.mode == 2 && *reinterpret_cast<volatile float*>(o.predictor) >= o.threshold);
-    uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {step start, last arrival, votes in, child launched, end}
+    uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {start, vote posted, votes in, -, last arrival, end}
     if (mark && blockIdx.x == 0 && threadIdx.x == 0) mark[0] = now_ns();
-    const double acc = norm_first ? norm_pass<4>(a.g, a.n, a.head)
-                                  : sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
+    if (norm_first) {
+        nf_body<MOM, NEST, W>(a, f, s, o, seq);
+        return;
+    }
+    // ---- update first: K13 over the whole buffer, vote in the last block
+    const double acc = sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
     Workspace ws = ws_view(f.ws);
     const double bsum = block_sum(acc);
     if (threadIdx.x == 0) {
@@ -200,39 +268,20 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
     for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
     v = block_sum(v);
     if (threadIdx.x != 0) return;
-    if (mark) mark[1] = now_ns();
     *ws.counter = 0u;
-    const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
     const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
     __threadfence_system();
     for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.rank, tagged);
-    bool to = false;
-    int w = 0;
-    for (int j = 0; j < s.world && !to; ++j) {
-        const uint64_t t = wait_tag(s.pads[s.rank] + j, seq, 32, s, &to);
-        const int wj = static_cast<int>(static_cast<uint32_t>(t));
-        w = wj > w ? wj : w;
-    }
-    if (to) {
-        atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
-        w = -1;
-    }
-    *f.word = w;
+    if (mark) mark[1] = now_ns();
+    const int w = agreed_vote(s, seq);
     if (mark) mark[2] = now_ns();
+    *f.word = w;
     if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
     const bool sync = w == SS_FLAG_SYNC;
     if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (sync ? 0.25f : 0.0f);
-    if (o.child_launches && (norm_first || sync)) atomicAdd(o.child_launches, 1u);
-    if (mark) mark[3] = now_ns();
-    if (norm_first) {
-        if (sync) {
-            upd_avg_kernel<MOM, NEST, W><<<gr.ua, kThreads, 0, cudaStreamTailLaunch>>>(a, s, o, seq, *o.epoch + 1);
-        } else {
-            update_kernel<MOM, NEST><<<gr.upd, kThreads, 0, cudaStreamTailLaunch>>>(a);
-            *s.seq = static_cast<uint32_t>(seq);
-        }
-    } else if (sync) {
+    if (sync) {
+        if (o.child_launches) atomicAdd(o.child_launches, 1u);
         avg_kernel<W><<<gr.avg, 512, 0, cudaStreamTailLaunch>>>(s, seq);
     } else {
         *s.seq = static_cast<uint32_t>(seq);
@@ -248,12 +297,10 @@ int occupancy(K kernel, int threads) {
 
 template <bool MOM, bool NEST, int W>
 int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, void* stream) {
-    static int res_step = 0, res_avg = 0, res_upd = 0, res_ua = 0;
+    static int res_step = 0, res_avg = 0;
     if (res_step == 0) {
         res_step = occupancy(step_kernel<MOM, NEST, W>, kThreads);
         res_avg = occupancy(avg_kernel<W>, 512);
-        res_upd = occupancy(update_kernel<MOM, NEST>, kThreads);
-        res_ua = occupancy(upd_avg_kernel<MOM, NEST, W>, kThreads);
     }
     const int sms = ss_internal::sm_count();
     const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res_step));
@@ -264,11 +311,11 @@ int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, v
     const int64_t per_rank_vec = ((sa.n >> 2) + sa.world - 1) / sa.world;
     const int64_t want = (per_rank_vec + 512 * 4 - 1) / (512 * 4);
     if (want < gr.avg) gr.avg = static_cast<int>(want < 1 ? 1 : want);
-    gr.upd = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res_upd));
-    gr.ua = sms * res_ua;
-    if (o.n_tiles * 2 < gr.ua) gr.ua = static_cast<int>(o.n_tiles * 2 > 0 ? o.n_tiles * 2 : 1);
-    // in-flight window ~ gr.ua tickets = gr.ua / (N + 1) groups: lag one window past it
-    o.lag = gr.ua / (sa.world + 1) + 2;
+    gr.upd = 0;
+    gr.ua = 0;
+    // norm-first pass: the in-flight window is ~grid tickets = grid / (N + 1)
+    // groups; the mean of a tile is scheduled one window after its update
+    o.lag = grid / (sa.world + 1) + 2;
     step_kernel<MOM, NEST, W><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, f, sa, o, gr);
     return check_launch("ss_step_symm_f32");
 }
@@ -323,6 +370,9 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
         o.tile = grp->tile_elems;
         o.n_tiles = tiles;
         o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
+        o.norm_done = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 192);
+        o.tile_norm = grp->tile_norm;
+        if (!o.tile_norm) return fail(SS_ERR_CONFIG, "norm-first order needs the per-tile norm buffer");
     }
     Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
     const bool mom = momentum != 0.0f, nest = nesterov != 0;

@@ -41,7 +41,7 @@ ev = ev[ev[:, 1] > 0]
 kind = ev[:, 0] >> 48
 t0 = ev[:, 1].min()
 out = {}
-for name, kk in (("update", 0), ("mean", 1)):
+for name, kk in (("norm", 2), ("update", 0), ("mean", 1)):
     e = ev[kind == kk]
     if len(e) == 0:
         continue
@@ -52,10 +52,8 @@ for name, kk in (("update", 0), ("mean", 1)):
 span = (ev[:, 3].max() - t0) / 1e3
 m0 = marks[0]
 lines = [f"rank {rank}: step {ms*1e3:.0f} us (events), overlapped kernel span {span:.0f} us",
-         "   step kernel: last block arrives {:.0f} us, votes in {:.0f}, child launched {:.0f}; "
-         "child first ticket {:.0f}; last arrival {:.0f}; end barrier done {:.0f} us".format(
-             (marks[1] - m0) / 1e3, (marks[2] - m0) / 1e3, (marks[3] - m0) / 1e3, (t0 - m0) / 1e3,
-             (marks[4] - m0) / 1e3, (marks[5] - m0) / 1e3)]
+         "   vote posted {:.0f} us; first ticket {:.0f}; last arrival {:.0f}; end barrier done {:.0f} us".format(
+             (marks[1] - m0) / 1e3, (t0 - m0) / 1e3, (marks[4] - m0) / 1e3, (marks[5] - m0) / 1e3)]
 for name, (n, wt, rn, first, last, p90) in out.items():
     lines.append(f"   {name:6s} tasks {n:5d}  wait {wt:7.1f} us  run {rn:7.1f} us (p90 {p90:.1f})  "
                  f"first start {first:7.0f} us  last end {last:7.0f} us")
