@@ -191,8 +191,9 @@ SS_API int ss_replica_flag_max_i32(int32_t* const* words_host, int32_t count, vo
 /* A rank's view of the symmetric (peer-mapped) parameter buffer and of every
    rank's signal region. Filled once by the host (e.g. from
    torch.distributed._symmetric_memory.rendezvous); all pointers are device
-   addresses valid in this process. The signal regions hold 2*world uint64
-   slots (ss_symm_signal_bytes) and must start zeroed on every rank. */
+   addresses valid in this process. The signal regions hold 3*world uint64
+   slots (ss_symm_signal_bytes: votes double-buffered by step parity + end-
+   barrier tags) and must start zeroed on every rank. */
 typedef struct ss_symm_group {
     float* bufs[SS_SYMM_MAX_RANKS];     /* rank r's flat fp32 buffer */
     uint64_t* pads[SS_SYMM_MAX_RANKS];  /* rank r's signal region */
@@ -225,7 +226,7 @@ typedef struct ss_symm_group {
     int64_t debug_cap;                  /* tickets recorded (4 x uint64 each) */
 } ss_symm_group;
 
-/* bytes of each rank's signal region (flag slots + done slots, uint64 each) */
+/* bytes of each rank's signal region (2 x world vote slots + world done slots, uint64 each) */
 SS_API int ss_symm_signal_bytes(int32_t world, int64_t* bytes_host);
 
 /* C2 (and optionally C1) as one launch after the update kernel:

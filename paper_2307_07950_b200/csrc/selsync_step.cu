@@ -81,9 +81,9 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
 
 // end of a sync step on this rank: done tags to every peer, wait for all
 __device__ void end_barrier(const SymmArgs& s, uint64_t seq) {
-    for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.world + s.rank, seq);
+    for (int j = 0; j < s.world; ++j) st_release_sys(done_slot(s, j, s.rank), seq);
     bool to = false;
-    for (int j = 0; j < s.world && !to; ++j) wait_tag(s.pads[s.rank] + s.world + j, seq, 0, s, &to);
+    for (int j = 0; j < s.world && !to; ++j) wait_tag(done_slot(s, s.rank, j), seq, 0, s, &to);
     if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
 }
 
@@ -104,7 +104,7 @@ __device__ int agreed_vote(const SymmArgs& s, uint64_t seq) {
     bool to = false;
     int w = 0;
     for (int j = 0; j < s.world && !to; ++j) {
-        const uint64_t t = wait_tag(s.pads[s.rank] + j, seq, 32, s, &to);
+        const uint64_t t = wait_tag(vote_slot(s, s.rank, seq, j), seq, 32, s, &to);
         const int wj = static_cast<int>(static_cast<uint32_t>(t));
         w = wj > w ? wj : w;
     }
@@ -163,7 +163,7 @@ __device__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, co
                     signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
                     const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
                     __threadfence_system();
-                    for (int j = 0; j < N; ++j) st_release_sys(s.pads[j] + s.rank, tagged);
+                    for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
                     if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
                 }
             }
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
     signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
     const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
     __threadfence_system();
-    for (int j = 0; j < s.world; ++j) st_release_sys(s.pads[j] + s.rank, tagged);
+    for (int j = 0; j < s.world; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
     if (mark) mark[1] = now_ns();
     const int w = agreed_vote(s, seq);
     if (mark) mark[2] = now_ns();

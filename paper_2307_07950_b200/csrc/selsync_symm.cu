@@ -44,7 +44,6 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     __shared__ int s_word;
     __shared__ bool s_timeout;
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(a.seq)) + 1;
-    uint64_t* my_pad = a.pads[a.rank];
     if (threadIdx.x == 0) {
         bool timed_out = false;
         int w;
@@ -53,11 +52,11 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
                 const int own = *a.word;
                 __threadfence_system();
                 const uint64_t v = (seq << 32) | static_cast<uint32_t>(own);
-                for (int j = 0; j < a.world; ++j) st_release_sys(a.pads[j] + a.rank, v);
+                for (int j = 0; j < a.world; ++j) st_release_sys(vote_slot(a, j, seq, a.rank), v);
             }
             w = 0;
             for (int j = 0; j < a.world && !timed_out; ++j) {
-                const uint64_t v = wait_tag(my_pad + j, seq, 32, a, &timed_out);
+                const uint64_t v = wait_tag(vote_slot(a, a.rank, seq, j), seq, 32, a, &timed_out);
                 const int wj = static_cast<int>(static_cast<uint32_t>(v));
                 w = wj > w ? wj : w;
             }
@@ -82,9 +81,9 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
             if (a.exchange) *a.word = w;
             if (a.agreed_ring && a.ring_cap > 0) a.agreed_ring[(seq - 1) % a.ring_cap] = s_timeout ? -1 : w;
             if (sync) {
-                for (int j = 0; j < a.world; ++j) st_release_sys(a.pads[j] + a.world + a.rank, seq);
+                for (int j = 0; j < a.world; ++j) st_release_sys(done_slot(a, j, a.rank), seq);
                 bool timed_out = false;
-                for (int j = 0; j < a.world && !timed_out; ++j) wait_tag(my_pad + a.world + j, seq, 0, a, &timed_out);
+                for (int j = 0; j < a.world && !timed_out; ++j) wait_tag(done_slot(a, a.rank, j), seq, 0, a, &timed_out);
                 if (timed_out) atomicExch(a.err, SS_SYMM_ERR_TIMEOUT);
             }
             *a.arrive = 0u;
@@ -145,7 +144,7 @@ extern "C" {
 int ss_symm_signal_bytes(int32_t world, int64_t* bytes) {
     if (!bytes) return fail(SS_ERR_CONFIG, "null output");
     if (world < 1 || world > kMaxRanks) return fail(SS_ERR_CONFIG, "world size must be in [1, %d], got %d", kMaxRanks, world);
-    *bytes = 2 * static_cast<int64_t>(world) * static_cast<int64_t>(sizeof(uint64_t));
+    *bytes = 3 * static_cast<int64_t>(world) * static_cast<int64_t>(sizeof(uint64_t));
     return SS_OK;
 }
 

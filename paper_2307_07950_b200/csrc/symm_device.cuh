@@ -14,7 +14,7 @@ namespace {
 constexpr int kMaxRanks = SS_SYMM_MAX_RANKS;
 struct SymmArgs {
     float* bufs[kMaxRanks];      // peer buffer bases, index = rank
-    uint64_t* pads[kMaxRanks];   // peer signal regions: [0, W) flag slots, [W, 2W) done slots
+    uint64_t* pads[kMaxRanks];   // peer signal regions: 2 x W vote slots (by seq parity), W done slots
     float* mc;                   // multicast address of the buffer, nullptr -> P2P path
     int rank, world;
     int64_t n;
@@ -83,6 +83,17 @@ __device__ uint64_t wait_tag(const uint64_t* p, uint64_t want, int shift, const 
         v = ld_acquire_sys(p);
     }
     return v;
+}
+
+// Signal slots of rank `owner`'s region. Votes are double-buffered by the
+// parity of the step tag: a fast rank may post its vote for step s+1 before a
+// slow rank has read the step-s votes, but never for s+2 (that needs the slow
+// rank's s+1 vote, posted only after it read all step-s votes).
+__device__ __forceinline__ uint64_t* vote_slot(const SymmArgs& a, int owner, uint64_t seq, int from) {
+    return a.pads[owner] + (seq & 1) * a.world + from;
+}
+__device__ __forceinline__ uint64_t* done_slot(const SymmArgs& a, int owner, int from) {
+    return a.pads[owner] + 2 * a.world + from;
 }
 
 __device__ __forceinline__ float4 scale4(float4 v, float s) {
