@@ -88,7 +88,6 @@ class SymmGroupC(Structure):
         ("tile_elems", c_int64),
         ("n_tiles", c_int64),
         ("child_launches", c_void_p),
-        ("tile_norm", c_void_p),
         ("debug_events", c_void_p),
         ("debug_cap", c_int64),
     ]

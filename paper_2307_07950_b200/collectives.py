@@ -181,8 +181,7 @@ class SymmetricParams:
         g.n_tiles = int(self.n_tiles)
         self.child_launches = torch.zeros(1, dtype=torch.int32, device=self.device)
         g.child_launches = self.child_launches.data_ptr()
-        self.tile_norm = torch.zeros(max(1, self.n_tiles), dtype=torch.float64, device=self.device)
-        g.tile_norm = self.tile_norm.data_ptr()
+
         self.group_c = g
         self.group_ref = ctypes.byref(g)
         torch.cuda.synchronize(self.device)

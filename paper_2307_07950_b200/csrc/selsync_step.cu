@@ -59,8 +59,6 @@ struct OverlapArgs {
     uint32_t* child_launches;  // optional launch counter (device-side launches)
     uint64_t* dbg;             // optional per-ticket timeline: {kind << 48 | tile, t0, t_ready, t_end}
     int64_t dbg_cap;
-    double* tile_norm;         // fp64 ||g_tile||^2 per tile (norm-first order)
-    unsigned int* norm_done;   // finished norm tiles (self-resetting)
 };
 
 struct Grids {
@@ -119,15 +117,43 @@ template <bool MOM, bool NEST, int W>
 __device__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o, uint64_t seq) {
     __shared__ unsigned long long s_ticket;
     __shared__ int s_vote;
-    __shared__ bool s_last_norm;
+    __shared__ bool s_last;
     const int N = s.world;
     const int64_t T = o.n_tiles;
     const int64_t groups = (T + N - 1) / N + o.lag;
-    const unsigned long long total = static_cast<unsigned long long>(T) + static_cast<unsigned long long>(groups) * (N + 1);
+    const unsigned long long total = static_cast<unsigned long long>(groups) * (N + 1);
     const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(o.epoch) + 1;
     const uint32_t target = static_cast<uint32_t>(N) * epoch;
     if (threadIdx.x == 0) s_vote = -2;
+    // ---- phase 1: ||g||^2 by the whole grid (full-speed sweep); the last block
+    //      to arrive reduces the partials in a fixed order, runs K2 and posts the
+    //      vote. Nobody waits here: blocks go straight on to the update tickets.
+    {
+        Workspace ws = ws_view(f.ws);
+        const double bsum = block_sum(norm_pass<4>(a.g, a.n, a.head));
+        if (threadIdx.x == 0) {
+            ws.partials[blockIdx.x] = bsum;
+            __threadfence();
+            s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            double v = 0.0;
+            for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
+            v = block_sum(v);
+            if (threadIdx.x == 0) {
+                *ws.counter = 0u;
+                signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+                const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+                __threadfence_system();
+                for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
+                if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
+            }
+        }
+    }
     __syncthreads();
+    // ---- phase 2: tickets -- groups of N update tiles + 1 mean of an owned tile
     for (;;) {
         if (threadIdx.x == 0) s_ticket = atomicAdd(o.ticket, 1ull);
         __syncthreads();
@@ -138,39 +164,8 @@ __device__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, co
         uint64_t t_start = rec ? now_ns() : 0, t_ready = 0;
         int64_t rec_tile = -1;
         int kind = 0;
-        if (k < static_cast<unsigned long long>(T)) {
-            // ---- norm tile k of the gradient
-            const int64_t t = static_cast<int64_t>(k);
-            const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
-            double acc = 0.0;
-            for (int64_t i = (e0 >> 2) + threadIdx.x; i < (e1 >> 2); i += blockDim.x) acc = sq4(ld_cs4(a.g + 4 * i), acc);
-            for (int64_t j = 4 * (e1 >> 2) + threadIdx.x; j < e1; j += blockDim.x)
-                acc = fma((double)a.g[j], (double)a.g[j], acc);
-            const double bsum = block_sum(acc);
-            if (threadIdx.x == 0) {
-                o.tile_norm[t] = bsum;
-                __threadfence();
-                s_last_norm = atomicAdd(o.norm_done, 1u) == static_cast<unsigned int>(T - 1);
-            }
-            __syncthreads();
-            if (s_last_norm) {  // every tile's partial is in: total in a fixed order, K2, vote
-                __threadfence();
-                double v = 0.0;
-                for (int64_t i = threadIdx.x; i < T; i += blockDim.x) v += __ldcg(o.tile_norm + i);
-                v = block_sum(v);
-                if (threadIdx.x == 0) {
-                    *o.norm_done = 0u;
-                    signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
-                    const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
-                    __threadfence_system();
-                    for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
-                    if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
-                }
-            }
-            kind = 2;
-            rec_tile = t;
-        } else {
-            const unsigned long long k2 = k - static_cast<unsigned long long>(T);
+        {
+            const unsigned long long k2 = k;
             const int64_t grp = static_cast<int64_t>(k2 / (N + 1));
             const int pos = static_cast<int>(k2 % (N + 1));
             if (pos < N) {
@@ -370,9 +365,6 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
         o.tile = grp->tile_elems;
         o.n_tiles = tiles;
         o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
-        o.norm_done = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 192);
-        o.tile_norm = grp->tile_norm;
-        if (!o.tile_norm) return fail(SS_ERR_CONFIG, "norm-first order needs the per-tile norm buffer");
     }
     Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
     const bool mom = momentum != 0.0f, nest = nesterov != 0;

@@ -41,7 +41,7 @@ ev = ev[ev[:, 1] > 0]
 kind = ev[:, 0] >> 48
 t0 = ev[:, 1].min()
 out = {}
-for name, kk in (("norm", 2), ("update", 0), ("mean", 1)):
+for name, kk in (("update", 0), ("mean", 1)):
     e = ev[kind == kk]
     if len(e) == 0:
         continue
