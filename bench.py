@@ -331,6 +331,19 @@ def main():
     # ---- headline: 50% sync mix, device-resident inputs
     mixed = make_step(0.3)
     run(mixed, args.warmup)
+    if world > 1 and args.collective == "symm":
+        # safety net: if the device-side exchange ever times out on this box,
+        # measure the NCCL back end instead of hanging the run
+        from paper_2307_07950_b200.errors import TransportError
+
+        try:
+            mixed.synchronize()
+        except TransportError as exc:
+            print(f"bench: symmetric-memory exchange failed ({exc}); falling back to NCCL",
+                  file=sys.stderr, flush=True)
+            args.collective = "nccl"
+            mixed = make_step(0.3)
+            run(mixed, args.warmup)
     clocks.start()
     res = timed(mixed, args.steps)
     clocks.stop()

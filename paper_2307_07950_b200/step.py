@@ -62,7 +62,7 @@ class SelSyncStep:
         trace_capacity: int = 4096,
         broadcast_init: bool = True,
         profile: bool = False,
-        timeout_s: float = 30.0,
+        timeout_s: float = 10.0,
         order: str = "adaptive",
         order_threshold: float = 0.3,
         tile_elems: int = 16384,
