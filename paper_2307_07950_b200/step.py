@@ -11,7 +11,8 @@ Device work per step, parameter aggregation (the default):
           fp64; the finishing block runs observe / relative_change / decide
           on the device-resident state and writes the int32 flag word
   C1      allreduce-MAX of the flag word = OR of the N votes (runtime.py:319-333)
-          -- NCCL (default) or the P2P exchange inside the C2 kernel
+          -- a seq-tagged P2P exchange over NVLink inside the step kernel
+          (default), or an NCCL allreduce-MAX of the word
   C2      sync steps only: the parameter mean (runtime.py:275-294)
 
 Back ends (N > 1):
