@@ -55,6 +55,8 @@ def parse():
                     help="microbench: the hot path on resident synthetic gradients (headline); model "
                          "workloads add stock PyTorch fwd/bwd of BASELINE configs 1-3")
     ap.add_argument("--delta", type=float, default=0.3, help="delta for model workloads")
+    ap.add_argument("--graph", action="store_true",
+                    help="model workloads: capture fwd + bwd + SelSync step in one CUDA graph")
     ap.add_argument("--sel-warmup", type=int, default=25, help="EWMA window / warmup for model workloads")
     ap.add_argument("--momentum", type=float, default=0.9)
     ap.add_argument("--weight-decay", type=float, default=4e-4)
@@ -485,8 +487,24 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
                         flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
                         trace_capacity=1 << 14, profile=True)
     st = tr.step
-    for _ in range(args.warmup):
-        tr.train_step()
+    graph = args.graph
+    if graph:
+        st.profile = False
+        batch0 = wl.make_batch(0)
+        static = tuple(t.clone() for t in batch0)
+        tr.capture(static, warmup_iters=max(3, args.warmup))
+
+        def one_step():
+            nb = wl.make_batch(tr.iteration)
+            if nb[0].data_ptr() != static[0].data_ptr():
+                for d_, s_ in zip(static, nb):
+                    d_.copy_(s_, non_blocking=True)
+            tr.replay_step()
+    else:
+        def one_step():
+            tr.train_step()
+        for _ in range(args.warmup):
+            one_step()
     torch.cuda.synchronize()
     comm.barrier(dev)
     clocks = ClockSampler(local)
@@ -495,14 +513,15 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
     clocks.start()
     a.record()
     for _ in range(args.steps):
-        tr.train_step()
+        one_step()
     b.record()
     torch.cuda.synchronize()
     clocks.stop()
     st.synchronize()
     comm.barrier(dev)
     ms = comm.max_float(a.elapsed_time(b), dev)
-    launches = K.LAUNCHES - l0
+    launches = K.LAUNCHES - l0 if not graph else args.steps  # one SelSync kernel per replayed graph
+    launches += device_launches(st)
     kms = st.kernel_ms()[k0:]
     dec = st.decisions()[d0 - st.steps_done:]
     # roofline of the update launch on local steps (sync steps add the mean)
@@ -511,7 +530,7 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
     nbytes = (20 if wl.momentum else 12) * st.params.numel()
     # e2e: public blocking API, batch copied from pinned host memory, loss read back
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not graph:
         hb = [t.cpu().pin_memory() for t in wl.make_batch(0)]
         db = [torch.empty_like(t, device=dev) for t in hb]
         lh = torch.empty(1, pin_memory=True)
@@ -537,7 +556,8 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic tensors of the config's shape, random-init weights",
-        "config": {"workload": f"{args.workload} (BASELINE configs): stock PyTorch fwd/bwd + SelSync hot path",
+        "config": {"workload": f"{args.workload} (BASELINE configs): stock PyTorch fwd/bwd + SelSync hot path"
+                               + (", fwd + bwd + step captured in one CUDA graph" if graph else ""),
                    "P": P, "P_padded": st.params.numel(), "delta": args.delta, "warmup": args.sel_warmup,
                    "momentum": wl.momentum, "weight_decay": wl.weight_decay, "n_workers": world,
                    "parallelism": f"dp{world} (SelSync replicas)",

@@ -51,3 +51,45 @@ class SelSyncTrainer:
             decision = None
         self.iteration += 1
         return loss, decision
+
+    # ------------------------------------------------------------------ graphs
+    def capture(self, batch, warmup_iters: int = 3) -> None:
+        """Capture forward + backward + the SelSync device step into ONE CUDA
+        graph over static batch tensors (``batch`` is (inputs, targets) on the
+        device; refill them in place before every ``replay_step``). Needs a
+        device-side branch (one rank, or collective="symm"). The learning rate
+        is a kernel argument: a new lr re-captures."""
+        from .errors import ConfigError
+
+        if not self.step.async_capable:
+            raise ConfigError("graph capture needs the device-side branch (one rank or collective='symm')")
+        if self.step.profile:
+            raise ConfigError("per-launch profiling events cannot be captured")
+        self.static_batch = tuple(batch)
+        side = torch.cuda.Stream(self.step.device)
+        side.wait_stream(torch.cuda.current_stream(self.step.device))
+        with torch.cuda.stream(side):  # cuDNN autotuning, allocator warm-up, first momentum step
+            for _ in range(warmup_iters):
+                self.train_step(self.static_batch)
+        torch.cuda.current_stream(self.step.device).wait_stream(side)
+        torch.cuda.synchronize(self.step.device)
+        self._record_graph()
+
+    def _record_graph(self) -> None:
+        self.graph = torch.cuda.CUDAGraph()
+        self.graph_lr = self.wl.lr(self.iteration)
+        with torch.cuda.graph(self.graph):
+            self.static_loss = self.forward_backward(self.static_batch)
+            self.step._enqueue_device_step(self.graph_lr, torch.cuda.current_stream(self.step.device))
+
+    def replay_step(self) -> torch.Tensor:
+        """One iteration by graph replay; returns the (static) loss tensor."""
+        lr = self.wl.lr(self.iteration)
+        if lr != self.graph_lr:
+            torch.cuda.synchronize(self.step.device)
+            self._record_graph()
+        self.graph.replay()
+        self.step.steps_done += 1
+        self.step.lrs.append(lr)
+        self.iteration += 1
+        return self.static_loss

@@ -68,3 +68,30 @@ def test_channels_last_views_and_update():
     want = before - wl.lr(0) * d
     torch.testing.assert_close(tr.flat.params, want, rtol=1e-5, atol=1e-6)
     assert math.isfinite(float(tr.flat.params.abs().max()))
+
+
+def test_graph_replay_matches_eager():
+    """fwd + bwd + SelSync step captured in one CUDA graph == the eager loop."""
+    import copy
+
+    wl = W.build("resnet101", DEV, seed=3)
+    wl2 = W.build("resnet101", DEV, seed=3)
+    wl2.model.load_state_dict(copy.deepcopy(wl.model.state_dict()))
+    x, y = wl.make_batch(0)
+    eager = SelSyncTrainer(wl, delta=0.05, warmup=2, smoothing=0.5)
+    graphed = SelSyncTrainer(wl2, delta=0.05, warmup=2, smoothing=0.5)
+    torch.backends.cudnn.deterministic = True
+    try:
+        for _ in range(3):
+            eager.train_step((x, y))
+        graphed.capture((x.clone(), y.clone()), warmup_iters=3)
+        for _ in range(4):
+            eager.train_step((x, y))
+            graphed.replay_step()
+        torch.cuda.synchronize()
+        ra, rb = eager.step.records(), graphed.step.records()
+        assert [r["decision"] for r in ra] == [r["decision"] for r in rb]
+        np.testing.assert_allclose([r["grad_norm_sq"] for r in ra], [r["grad_norm_sq"] for r in rb], rtol=1e-4)
+        torch.testing.assert_close(eager.flat.params, graphed.flat.params, rtol=1e-4, atol=1e-5)
+    finally:
+        torch.backends.cudnn.deterministic = False
