@@ -526,8 +526,9 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
     dec = st.decisions()[d0 - st.steps_done:]
     # roofline of the update launch on local steps (sync steps add the mean)
     local_ms = [t for t, d in zip(kms, dec) if not d] if world > 1 else kms
-    k_mean = sum(local_ms) / len(local_ms) if local_ms else float("nan")
+    k_mean = sum(local_ms) / len(local_ms) if local_ms else None
     nbytes = (20 if wl.momentum else 12) * st.params.numel()
+    achieved = nbytes / (k_mean * 1e-3) / 1e9 if k_mean else None
     # e2e: public blocking API, batch copied from pinned host memory, loss read back
     e2e = None
     if not args.no_e2e and not graph:
@@ -564,10 +565,12 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
                    "value_counts": "worker-steps: N ranks x K steps / (max-over-ranks device time)"},
         "observed_sync_frac": sum(dec) / max(1, len(dec)),
         "roofline": {"bound": "hbm", "kernel": "SelSync update launch (K13+K2[+exchange])",
-                     "achieved": nbytes / (k_mean * 1e-3) / 1e9, "peak": hbm_peak, "peak_source": hbm_src,
-                     "unit": "GB/s", "frac": nbytes / (k_mean * 1e-3) / 1e9 / hbm_peak, "traffic": None,
-                     "kernel_ms_mean": k_mean, "timed_on": "local steps" if world > 1 else "all steps",
-                     "hot_path_share_of_step": sum(kms) / len(kms) / (ms / args.steps)},
+                     "achieved": achieved, "peak": hbm_peak, "peak_source": hbm_src,
+                     "unit": "GB/s", "frac": achieved / hbm_peak if achieved else None, "traffic": None,
+                     "kernel_ms_mean": k_mean,
+                     "timed_on": ("not timed inside a CUDA graph (run without --graph)" if graph else
+                                  "local steps" if world > 1 else "all steps"),
+                     "hot_path_share_of_step": sum(kms) / len(kms) / (ms / args.steps) if kms else None},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
