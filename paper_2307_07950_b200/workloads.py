@@ -69,7 +69,8 @@ class TransformerLM(nn.Module):
         if self.mask.size(0) != n:
             self.mask = torch.triu(torch.full((n, n), float("-inf"), device=src.device), diagonal=1)
         x = self.pos(self.encoder(src) * math.sqrt(self.d_model))
-        return self.decoder(self.transformer(x, self.mask))
+        # is_causal: skip the mask inspection (a host sync that would break graph capture)
+        return self.decoder(self.transformer(x, self.mask, is_causal=True))
 
 
 @dataclass
