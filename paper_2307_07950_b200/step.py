@@ -168,14 +168,12 @@ class SelSyncStep:
         if ev:
             ev[0].record(stream)
         if self.collective == "symm" and self.flag_exchange == "fused":
-            # one cooperative launch: update, norm, vote, vote exchange, conditional mean
-            K.step_symm_(self.params, self.grads, self.momentum, self.signal, self.ws, self.symm,
-                         lr=lr, delta=cfg.delta, **self._hp(self.steps_done == 0))
+            # one host launch: update, norm, vote, vote exchange, conditional mean
+            self._fast_launch("symm", lr, stream)
             if ev:
                 ev[1].record(stream)
             return
-        K.update_norm_signal_(self.params, self.grads, self.momentum, self.signal, self.ws,
-                              lr=lr, delta=cfg.delta, **self._hp(self.steps_done == 0))
+        self._fast_launch("k13", lr, stream)
         if ev:
             ev[1].record(stream)
         if self.collective == "symm":
@@ -189,6 +187,38 @@ class SelSyncStep:
             K._count()
             if ev:
                 ev[1].record(stream)
+
+    def _fast_launch(self, which: str, lr: float, stream) -> None:
+        """Launch K13+K2 (or the one-launch symmetric step) with an argument
+        tuple validated once: only the gradient pointer (the caller may rebind
+        ``grads``), lr, the first-step flag and the stream change per step.
+        At small P a step is shorter than the Python launch path; this keeps
+        that path to one ctypes call."""
+        from . import _native as N
+
+        key = (which, self.grads.data_ptr(), self.grads.numel())
+        if getattr(self, "_fast_key", None) != key:
+            # full validation whenever the bound gradient changes
+            K._sgd_check(self.params, self.grads, self.momentum, self.config.momentum)
+            c = self.config
+            m = self.momentum.data_ptr() if self.momentum is not None else None
+            head = [self.params.data_ptr(), self.grads.data_ptr(), m, self.params.numel()]
+            hp = [float(c.momentum), float(c.dampening), float(c.weight_decay), int(bool(c.nesterov))]
+            tail = [self.signal.state.data_ptr(), float(c.delta), self.signal.word.data_ptr(),
+                    self.signal.trace.data_ptr(), self.signal.trace_capacity]
+            if which == "symm":
+                self._fast_fn = N.LIB.ss_step_symm_f32
+                tail += [self.symm.group_ref, self.ws.ptr]
+            else:
+                self._fast_fn = N.LIB.ss_update_norm_signal_f32
+                tail += [self.ws.ptr]
+            self._fast_parts = (head, hp, tail)
+            self._fast_key = key
+        head, hp, tail = self._fast_parts
+        rc = self._fast_fn(*head, lr, *hp, int(self.steps_done == 0), *tail, stream.cuda_stream)
+        if rc:
+            N.check(rc)
+        K._count()
 
     def step_async(self, lr: float) -> None:
         """Enqueue one whole step and return without waiting for the GPU.
