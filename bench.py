@@ -190,7 +190,8 @@ def cpu_run(n_workers, P, steps, warmup, args, budget_s):
         "sample": (f"{steps} timed steps of the reference's float64 SelSync step (oracle/cpu_path.py: "
                    f"g@g, observe/decide, SGD+momentum+wd, flag OR, on sync f64 serialize + PS "
                    f"np.stack().mean + deserialize) for {n_workers} worker(s) at P_sample={p_sample:,} "
-                   f"({syncs}/{steps} sync steps), scaled x{P / p_sample:.2f} to P={P:,}"),
+                   f"({syncs}/{steps} sync steps), vectors sliced over {threads} host threads, "
+                   f"time scaled x{P / p_sample:.2f} to P={P:,}"),
         "sec_per_step_sample": secs / steps,
     }
 
