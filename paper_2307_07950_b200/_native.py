@@ -8,7 +8,6 @@ CUDA tensor. Build it with ``python -m paper_2307_07950_b200._build``.
 from __future__ import annotations
 
 import ctypes
-import math
 from ctypes import (
     POINTER,
     Structure,
@@ -196,6 +195,3 @@ def ptr_array(ptrs) -> ctypes.Array:
         arr[i] = p
     return arr
 
-
-def nan() -> float:
-    return math.nan

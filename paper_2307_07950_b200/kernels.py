@@ -9,7 +9,6 @@ this module (bench.py reports it as ``gpu_launches``).
 from __future__ import annotations
 
 import ctypes
-import math
 from typing import Optional, Sequence
 
 import numpy as np
@@ -252,15 +251,11 @@ def replica_flag_max_(words: Sequence[torch.Tensor]) -> None:
 
 
 def raise_for_word(word: int, where: str = "") -> None:
-    """Turn the error bits of an agreed flag word into the reference's SignalError."""
-    if word & N.SS_FLAG_ERR_NAN or (word >= 2 and not word & N.SS_FLAG_ERR_NEG):
-        raise SignalError(f"observed a NaN gradient norm{where}")
-    if word & N.SS_FLAG_ERR_NEG:
+    """Turn the error bits of an agreed flag word (>= 2) into the reference's
+    SignalError (signal.py:67-70); a NaN anywhere wins over a negative."""
+    if word & N.SS_FLAG_ERR_NEG and not word & N.SS_FLAG_ERR_NAN:
         raise SignalError(f"squared norm cannot be negative{where}")
-
-
-def isnan(x: float) -> bool:
-    return isinstance(x, float) and math.isnan(x)
+    raise SignalError(f"observed a NaN gradient norm{where}")
 
 
 def step_symm_(w, g, m, signal: DeviceSignal, ws: Workspace, group, *, lr: float, delta: float,

@@ -1,4 +1,6 @@
-"""Replay the n4_mixed golden case through each order; report the first timeout."""
+"""Stress of the device-side exchange: replay the n4_mixed golden case through
+each step order with back-to-back async steps and pinned H2D copies (the
+scenario that exposed the single-buffered vote slots); report timeouts."""
 import os
 import sys
 from pathlib import Path
