@@ -46,9 +46,12 @@ __version__ = "0.1.0"
 
 def __getattr__(name):
     # torch-dependent parts load lazily so the scalar API imports fast
-    if name in ("SelSyncStep",):
-        from .step import SelSyncStep
-        return SelSyncStep
+    if name in ("SelSyncStep", "TensorListSelSyncStep"):
+        from . import step
+        return getattr(step, name)
+    if name in ("SelSyncTrainer",):
+        from .train import SelSyncTrainer
+        return SelSyncTrainer
     if name in ("ReplicaSelSync",):
         from .replicas import ReplicaSelSync
         return ReplicaSelSync

@@ -64,3 +64,14 @@ def test_int_max_equals_bit_or():
 
     for votes in itertools.product([0, 1], repeat=5):
         assert (max(votes) == 1) == any_flag(votes_to_word(votes))
+
+
+def test_integration_doc_names_resolve():
+    """Every name INTEGRATION.md imports from the package resolves (lazily)."""
+    import paper_2307_07950_b200 as S
+
+    for name in ("observe", "decide", "DeltaThreshold", "GradSignalState", "default_smoothing",
+                 "SelSyncConfig", "split_chunks", "plan_seldp", "bind_plan", "ChunkSampler",
+                 "FlatParameters", "SelSyncStep", "LrSchedule", "lr_at", "SelSyncTrainer",
+                 "TensorListSelSyncStep", "ReplicaSelSync", "RankGroup"):
+        assert getattr(S, name) is not None, name
