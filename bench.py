@@ -92,7 +92,7 @@ class ClockSampler:
     REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index: int, period_s: float = 0.01):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.samples = []
         self.ok = False
         self.period = period_s
@@ -229,13 +229,15 @@ def workload_config(args, world):
                      f"{args.weight_decay}, 50% sync decision mix"),
         "P": args.P,
         "n_workers": world,
-        "order": "prescale" if args.no_fuse else "fused",
+        "update_kernel": "K1+K2 then K3 with 1/N pre-scale" if args.no_fuse else "fused K13+K2",
         "collective": args.collective if world > 1 else "none (single rank)",
         "flag_exchange": args.flag_exchange if world > 1 else "none (single rank)",
         "step_order": args.order if world > 1 and args.flag_exchange == "fused" else "update_first",
         "decision_mix": {"sync_frac": 0.5, "grad_scales": MIX_SCALES, "smoothing": 1.0, "delta": 0.3,
                          "warmup": 1},
-        "parallelism": f"dp{world} (SelSync replicas, NCCL)",
+        "parallelism": (f"dp{world} (SelSync replicas; vote + mean over "
+                        + ("NVLink symmetric memory" if args.collective == "symm" else "NCCL") + ")"
+                        if world > 1 else "dp1 (single replica, no exchange)"),
         "value_counts": "worker-steps: N ranks x K steps / (max-over-ranks device time)",
         "l2": f"inputs exceed L2: w, g, m = {12 * args.P / 1e9:.2f} GB per step vs 126 MB L2",
     }
