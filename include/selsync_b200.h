@@ -255,6 +255,18 @@ SS_API int ss_step_symm_f32(float* w_dev, const float* g_dev, float* m_dev, int6
                             int32_t* word_dev, ss_trace_row* trace_dev, int32_t trace_cap,
                             const ss_symm_group* g_host, void* ws_dev, void* stream);
 
+/* The gradient-aggregation step in one launch (strategies.py:395-399 with
+   the server's GA round, runtime.py:259-273): ||g||^2 + vote, then on sync
+   the mean GRADIENT over ranks (tile by tile, NVLS / P2P) and the update with
+   it; on local steps the update with the own gradient. g_dev must be
+   g_host->bufs[g_host->rank] (the gradient lives in symmetric memory);
+   needs tile_cnt / epoch / tile_elems of the group. */
+SS_API int ss_step_symm_ga_f32(float* w_dev, float* g_dev, float* m_dev, int64_t n, float lr,
+                               float momentum, float dampening, float weight_decay, int32_t nesterov,
+                               int32_t first_step, ss_signal_state* st_dev, double delta,
+                               int32_t* word_dev, ss_trace_row* trace_dev, int32_t trace_cap,
+                               const ss_symm_group* g_host, void* ws_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

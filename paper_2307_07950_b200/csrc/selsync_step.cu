@@ -283,6 +283,112 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
     }
 }
 
+// ------------------------------------------- gradient aggregation, one launch
+//
+// _selsync_step with aggregation="grads" (strategies.py:395-399): the vote
+// precedes the update, and on sync the update uses the MEAN gradient
+// (runtime.py:259-273 does not store it). The flat gradient buffer lives in
+// symmetric memory. ||g||^2 sweep + vote (as in the norm-first pass), then
+// tickets: the mean of one tile this rank owns (NVLS / P2P, written back into
+// every rank's gradient, then announced to every rank by a remote atomic
+// add), followed `lag` groups later by N tile updates, each of which -- on a
+// sync step -- waits for its tile's announcement. On a local step no ticket
+// waits and the update uses the rank's own gradient.
+template <bool MOM, bool NEST, int W>
+__global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
+    __shared__ unsigned long long s_ticket;
+    __shared__ int s_vote;
+    __shared__ bool s_last;
+    const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
+    const int N = s.world;
+    const int64_t T = o.n_tiles;
+    const int64_t groups = (T + N - 1) / N + o.lag;
+    const unsigned long long total = static_cast<unsigned long long>(groups) * (N + 1);
+    const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(o.epoch) + 1;  // sync steps so far + 1
+    if (threadIdx.x == 0) s_vote = -2;
+    {   // ---- ||g||^2 sweep; the last block runs K2 and posts the vote
+        Workspace ws = ws_view(f.ws);
+        const double bsum = block_sum(norm_pass<4>(a.g, a.n, a.head));
+        if (threadIdx.x == 0) {
+            ws.partials[blockIdx.x] = bsum;
+            __threadfence();
+            s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            double v = 0.0;
+            for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
+            v = block_sum(v);
+            if (threadIdx.x == 0) {
+                *ws.counter = 0u;
+                signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+                const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+                __threadfence_system();
+                for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
+            }
+        }
+    }
+    __syncthreads();
+    // every ticket needs the branch: the agreed vote (all ranks finished their sweep)
+    if (threadIdx.x == 0) s_vote = agreed_vote(s, seq);
+    __syncthreads();
+    const bool sync = s_vote == SS_FLAG_SYNC;
+    for (;;) {
+        if (threadIdx.x == 0) s_ticket = atomicAdd(o.ticket, 1ull);
+        __syncthreads();
+        const unsigned long long k = s_ticket;
+        __syncthreads();
+        if (k >= total) break;
+        const int64_t grp = static_cast<int64_t>(k / (N + 1));
+        const int pos = static_cast<int>(k % (N + 1));
+        if (pos == 0) {
+            // ---- mean of owned tile t = grp*N + rank, then announce it to every rank
+            const int64_t t = grp * N + s.rank;
+            if (sync && t < T) {
+                const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
+                average_block_range<W>(s, e0, e1);
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence_system();
+                    for (int j = 0; j < N; ++j) red_add_release_sys(o.cnt[j] + t, 1u);
+                }
+            }
+        } else {
+            // ---- update tile t of group grp - lag (owner t % N), with the mean gradient on sync
+            const int64_t t = (grp - o.lag) * N + (pos - 1);
+            if (grp >= o.lag && t < T) {
+                if (sync && threadIdx.x == 0) {
+                    const uint64_t t0 = now_ns();
+                    while (static_cast<int32_t>(ld_acquire_sys_u32(o.cnt[s.rank] + t) - epoch) < 0) {
+                        if (now_ns() - t0 > s.timeout_ns) {
+                            atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+                            break;
+                        }
+                        __nanosleep(128);
+                    }
+                }
+                __syncthreads();
+                const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
+                sgd_block_range<MOM, NEST, 2, true>(a, e0, e1);
+            }
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+        *f.word = s_vote;
+        if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = s_vote;
+        if (sync) {
+            end_barrier(s, seq);  // no rank reuses its gradient buffer while a peer still reads it
+            *o.epoch = epoch;
+        }
+        *o.ticket = 0ull;
+        *s.arrive = 0u;
+        *s.seq = static_cast<uint32_t>(seq);
+    }
+}
+
 template <typename K>
 int occupancy(K kernel, int threads) {
     int x = 0;
@@ -321,6 +427,26 @@ int dispatch_step(const SgdArgs& a, const Finish& f, const SymmArgs& sa, const O
     if (!mom) return launch_step<false, false, W>(a, f, sa, o, stream);
     if (nest) return launch_step<true, true, W>(a, f, sa, o, stream);
     return launch_step<true, false, W>(a, f, sa, o, stream);
+}
+
+
+template <bool MOM, bool NEST, int W>
+int launch_step_ga(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, void* stream) {
+    static int res = 0;
+    if (res == 0) res = occupancy(step_ga_kernel<MOM, NEST, W>, kThreads);
+    const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res));
+    f.total_blocks = grid;
+    o.lag = grid / (sa.world + 1) + 2;
+    step_ga_kernel<MOM, NEST, W><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, f, sa, o);
+    return check_launch("ss_step_symm_ga_f32");
+}
+
+template <int W>
+int dispatch_step_ga(const SgdArgs& a, const Finish& f, const SymmArgs& sa, const OverlapArgs& o, bool mom,
+                     bool nest, void* stream) {
+    if (!mom) return launch_step_ga<false, false, W>(a, f, sa, o, stream);
+    if (nest) return launch_step_ga<true, true, W>(a, f, sa, o, stream);
+    return launch_step_ga<true, false, W>(a, f, sa, o, stream);
 }
 
 }  // namespace
@@ -375,5 +501,51 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
         case 8: return dispatch_step<8>(a, f, sa, o, mom, nest, stream);
         default:
             return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 2, 4, 8)", sa.world);
+    }
+}
+
+extern "C" int ss_step_symm_ga_f32(float* w, float* g, float* m, int64_t n, float lr, float momentum,
+                                   float dampening, float weight_decay, int32_t nesterov, int32_t first_step,
+                                   ss_signal_state* st, double delta, int32_t* word, ss_trace_row* trace,
+                                   int32_t cap, const ss_symm_group* grp, void* ws, void* stream) {
+    SgdArgs a;
+    int rc = make_sgd_args(&a, w, g, m, n, lr, momentum, dampening, weight_decay, nesterov, first_step,
+                           nullptr, 1.0f);
+    if (rc) return rc;
+    if (!st || !ws || !word) return fail(SS_ERR_CONFIG, "null state/word/workspace");
+    rc = check_delta_impl(delta);
+    if (rc) return rc;
+    rc = check_trace(trace, cap);
+    if (rc) return rc;
+    SymmArgs sa;
+    rc = symm_args_from_group(grp, n, word, 1, 1.0f / static_cast<float>(grp ? grp->world : 1), ws, &sa,
+                              &ss_internal::fail);
+    if (rc) return rc;
+    if (grp->bufs[grp->rank] != g) return fail(SS_ERR_CONFIG, "g must be this rank's symmetric buffer");
+    if (a.head != 0) return fail(SS_ERR_CONFIG, "gradient aggregation needs 16-byte aligned w, g, m");
+    if (!grp->epoch || grp->tile_elems <= 0 || (grp->tile_elems & 3))
+        return fail(SS_ERR_CONFIG, "gradient aggregation needs epoch and a tile size (multiple of 4)");
+    OverlapArgs o{};
+    const int64_t tiles = (n + grp->tile_elems - 1) / grp->tile_elems;
+    if (tiles > grp->n_tiles) return fail(SS_ERR_CONFIG, "tile counters hold %lld tiles, need %lld",
+                                         (long long)grp->n_tiles, (long long)tiles);
+    for (int r = 0; r < kMaxRanks; ++r) {
+        if (r < grp->world && !grp->tile_cnt[r]) return fail(SS_ERR_CONFIG, "null tile counters for rank %d", r);
+        o.cnt[r] = r < grp->world ? grp->tile_cnt[r] : nullptr;
+    }
+    o.epoch = grp->epoch;
+    o.predictor = grp->predictor;
+    o.tile = grp->tile_elems;
+    o.n_tiles = tiles;
+    o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
+    Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
+    const bool mom = momentum != 0.0f, nest = nesterov != 0;
+    switch (symm_width(sa)) {
+        case 0: return dispatch_step_ga<0>(a, f, sa, o, mom, nest, stream);
+        case 2: return dispatch_step_ga<2>(a, f, sa, o, mom, nest, stream);
+        case 4: return dispatch_step_ga<4>(a, f, sa, o, mom, nest, stream);
+        case 8: return dispatch_step_ga<8>(a, f, sa, o, mom, nest, stream);
+        default:
+            return fail(SS_ERR_CONFIG, "gradient aggregation: world %d needs multicast (P2P widths 2, 4, 8)", sa.world);
     }
 }

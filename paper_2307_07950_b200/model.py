@@ -163,5 +163,14 @@ class FlatParameters:
             p.data = self._view(params, off, shape, cl)
         self.params = params
 
+    def rebind_grads(self, grads: torch.Tensor) -> None:
+        """Point every ``p.grad`` at views of another flat buffer (e.g. the
+        symmetric-memory gradient of a gradient-aggregation SelSyncStep)."""
+        if grads.numel() != self.numel or grads.dtype != torch.float32:
+            raise ConfigError("rebind_grads needs a flat fp32 buffer of the same padded size")
+        for p, (off, shape), cl in zip(self.parameters, self.layout, self.channels_last):
+            p.grad = self._view(grads, off, shape, cl)
+        self.grads = grads
+
     def vector(self) -> ParamVector:
         return ParamVector(self.params, self.layout)

@@ -89,13 +89,14 @@ class SelSyncStep:
             flag_exchange = "fused" if collective == "symm" else "nccl"
         if flag_exchange not in ("nccl", "p2p", "fused"):
             raise ConfigError(f"flag_exchange must be 'fused', 'p2p' or 'nccl', got {flag_exchange!r}")
-        if collective == "symm" and config.aggregation != "params":
-            raise ConfigError("the symmetric-memory exchange implements parameter aggregation")
         if flag_exchange in ("p2p", "fused") and collective != "symm" and self.world > 1:
             raise ConfigError("the P2P flag exchange runs inside the symmetric-memory kernels")
         self.collective = collective if self.world > 1 else "none"
         self.flag_exchange = flag_exchange
         self.fuse = (bool(fuse) or self.collective == "symm") and config.aggregation == "params"
+        if self.collective == "symm" and config.aggregation == "grads" and flag_exchange != "fused":
+            raise ConfigError("gradient aggregation over symmetric memory is the one-launch step "
+                              "(flag_exchange='fused')")
         if config.momentum != 0.0:
             if momentum_buffer is None:
                 momentum_buffer = torch.zeros_like(params)
@@ -112,10 +113,18 @@ class SelSyncStep:
                                         ring_capacity=trace_capacity, timeout_s=timeout_s,
                                         order=order, order_threshold=order_threshold,
                                         tile_elems=tile_elems)
-            self.symm.buf.copy_(params)
-            params = self.symm.buf  # the step owns the symmetric copy; use step.params
-            if self.flag_exchange == "fused" and not self.symm.one_launch_capable:
-                self.flag_exchange = "p2p"
+            if config.aggregation == "grads":
+                # the exchanged vector is the gradient: it lives in symmetric memory
+                self.symm.buf.copy_(grads)
+                self.grads = self.symm.buf  # backward must write step.grads
+                if not self.symm.one_launch_capable:
+                    raise ConfigError(f"gradient aggregation over symmetric memory needs multicast or "
+                                      f"2, 4 or 8 ranks (world {self.world})")
+            else:
+                self.symm.buf.copy_(params)
+                params = self.symm.buf  # the step owns the symmetric copy; use step.params
+                if self.flag_exchange == "fused" and not self.symm.one_launch_capable:
+                    self.flag_exchange = "p2p"
         self.params = params
         self._word_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._ready = torch.cuda.Event()
@@ -169,7 +178,7 @@ class SelSyncStep:
             ev[0].record(stream)
         if self.collective == "symm" and self.flag_exchange == "fused":
             # one host launch: update, norm, vote, vote exchange, conditional mean
-            self._fast_launch("symm", lr, stream)
+            self._fast_launch("symm_ga" if cfg.aggregation == "grads" else "symm", lr, stream)
             if ev:
                 ev[1].record(stream)
             return
@@ -206,8 +215,8 @@ class SelSyncStep:
             hp = [float(c.momentum), float(c.dampening), float(c.weight_decay), int(bool(c.nesterov))]
             tail = [self.signal.state.data_ptr(), float(c.delta), self.signal.word.data_ptr(),
                     self.signal.trace.data_ptr(), self.signal.trace_capacity]
-            if which == "symm":
-                self._fast_fn = N.LIB.ss_step_symm_f32
+            if which in ("symm", "symm_ga"):
+                self._fast_fn = N.LIB.ss_step_symm_f32 if which == "symm" else N.LIB.ss_step_symm_ga_f32
                 tail += [self.symm.group_ref, self.ws.ptr]
             else:
                 self._fast_fn = N.LIB.ss_update_norm_signal_f32

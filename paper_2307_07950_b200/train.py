@@ -29,6 +29,8 @@ class SelSyncTrainer:
         self.step = SelSyncStep(self.flat.params, self.flat.grads, cfg, group=group, **step_kw)
         if self.step.params.data_ptr() != self.flat.params.data_ptr():
             self.flat.rebind(self.step.params)  # parameters now live in symmetric memory
+        if self.step.grads.data_ptr() != self.flat.grads.data_ptr():
+            self.flat.rebind_grads(self.step.grads)  # gradient aggregation: grads in symmetric memory
         self.iteration = 0
 
     def forward_backward(self, batch=None) -> torch.Tensor:

@@ -130,6 +130,7 @@ CASES = {
     "n4_delta0": (4, 100, 30, 0.0, 1, None, 0.1, "params", 5),
     "n4_huge": (4, 100, 40, 1e9, 5, None, 0.1, "params", 6),
     "n4_grads": (4, 300, 50, 0.02, 5, None, 0.1, "grads", 7),
+    "n2_grads": (2, 301, 50, 0.05, 3, 0.5, 0.1, "grads", 8),
 }
 
 

@@ -47,11 +47,12 @@ def main():
     g = torch.zeros(P, device=dev)
     cfg = SelSyncConfig(delta=c["delta"], aggregation=c["aggregation"], warmup=c["warmup"],
                         smoothing=c["smoothing"])
-    if c["aggregation"] != "params" and opts["collective"] == "symm":
+    if c["aggregation"] != "params" and opts["collective"] == "symm" and opts.get("flag_exchange") != "fused":
         opts = dict(collective="nccl", fuse=True)
     step = SelSyncStep(init, g, cfg, **opts)
     host = [torch.from_numpy(O.synthetic_grad32(c["grad_seed"], rank, s, P)).pin_memory()
             for s in range(c["steps"])]
+    g = step.grads  # gradient aggregation over symmetric memory owns the gradient buffer
     for s in range(c["steps"]):
         g.copy_(host[s], non_blocking=True)
         if step.async_capable and s % 2:

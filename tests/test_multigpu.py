@@ -29,7 +29,7 @@ def run_torchrun(n, name, mode, out):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("name,n", [("n2_lam0.5", 2), ("cfg0_n2_d0.3", 2), ("n4_mixed", 4),
+@pytest.mark.parametrize("name,n", [("n2_lam0.5", 2), ("cfg0_n2_d0.3", 2), ("n2_grads", 2), ("n4_mixed", 4),
                                     ("n4_grads", 4), ("n8_mixed", 8)])
 @pytest.mark.parametrize("mode", ["fused", "prescale", "symm-nccl", "symm-p2p", "symm-fused",
                                   "symm-normfirst", "symm-adaptive"])
