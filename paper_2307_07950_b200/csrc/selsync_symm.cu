@@ -39,7 +39,7 @@ namespace {
 
 constexpr int kThreads = 512;
 
-template <int W, int UO = 0>
+template <int W, int UO = 0, int LS = 0>
 __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     __shared__ int s_word;
     __shared__ bool s_timeout;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     const int w = s_word;
     const bool sync = !s_timeout && w == SS_FLAG_SYNC;
     if (sync) {
-        average_shard<W, UO>(a);
+        average_shard<W, UO, LS>(a);
         __threadfence_system();
     }
     __syncthreads();
@@ -92,12 +92,12 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     }
 }
 
-template <int W, int UO = 0>
+template <int W, int UO = 0, int LS = 0>
 int launch_symm_u(const SymmArgs& a, cudaStream_t s) {
     static int resident = 0;
     if (resident == 0) {
         int x = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, symm_sync_kernel<W, UO>, kThreads, 0) != cudaSuccess || x <= 0) x = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, symm_sync_kernel<W, UO, LS>, kThreads, 0) != cudaSuccess || x <= 0) x = 1;
         resident = x;
     }
     // all blocks co-resident: they never wait on each other, but the last
@@ -112,7 +112,7 @@ int launch_symm_u(const SymmArgs& a, cudaStream_t s) {
     const int64_t per_rank_vec = ((a.n >> 2) + a.world - 1) / a.world;
     const int64_t want = (per_rank_vec + kThreads * 4 - 1) / (kThreads * 4);
     if (want < grid) grid = static_cast<int>(want < 1 ? 1 : want);
-    symm_sync_kernel<W, UO><<<grid, kThreads, 0, s>>>(a);
+    symm_sync_kernel<W, UO, LS><<<grid, kThreads, 0, s>>>(a);
     return ss_internal::check_launch("ss_symm_sync_f32");
 }
 
@@ -124,6 +124,19 @@ int launch_symm(const SymmArgs& a, cudaStream_t s) {
     if (u < 0) {
         const char* e = getenv("SS_SYMM_UNROLL");
         u = e ? atoi(e) : 0;
+    }
+    static int ls = -1;
+    if (ls < 0) {
+        const char* e = getenv("SS_P2P_VARIANT");
+        ls = e ? atoi(e) : 0;
+    }
+    if constexpr (W == 2) {
+        switch (ls) {
+            case 1: return launch_symm_u<W, 0, 1>(a, s);
+            case 2: return launch_symm_u<W, 0, 2>(a, s);
+            case 3: return launch_symm_u<W, 0, 3>(a, s);
+            default: break;
+        }
     }
     if constexpr (W == 0 || W == 2 || W == 4 || W == 8) {
         switch (u) {

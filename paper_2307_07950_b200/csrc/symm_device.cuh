@@ -96,6 +96,20 @@ __device__ __forceinline__ uint64_t* done_slot(const SymmArgs& a, int owner, int
     return a.pads[owner] + 2 * a.world + from;
 }
 
+// peer load / store flavours of the P2P mean (tuning: SS_P2P_VARIANT)
+template <int LS>
+__device__ __forceinline__ float4 p2p_ld(const float4* p) {
+    if constexpr (LS == 1) return *p;
+    else if constexpr (LS == 3) return __ldcs(p);
+    else return __ldcg(p);
+}
+template <int LS>
+__device__ __forceinline__ void p2p_st(float4* p, float4 v) {
+    if constexpr (LS == 1) *p = v;
+    else if constexpr (LS == 2 || LS == 3) __stcs(p, v);
+    else __stcg(p, v);
+}
+
 __device__ __forceinline__ float4 scale4(float4 v, float s) {
     v.x *= s; v.y *= s; v.z *= s; v.w *= s;
     return v;
@@ -174,7 +188,7 @@ __device__ __forceinline__ void shard_range(const SymmArgs& a, int64_t* v0, int6
 // NVLS: the switch reduces, multimem.st broadcasts (W = 0) -- or P2P two-shot
 // over W peers: all W loads of U vectors issued before any add (fixed rank
 // order => every rank's copy of a shard is bit-identical).
-template <int W, int UO = 0>
+template <int W, int UO = 0, int LS = 0>
 __device__ void average_shard(const SymmArgs& a) {
     int64_t v0, v1;
     shard_range(a, &v0, &v1);
@@ -210,7 +224,7 @@ __device__ void average_shard(const SymmArgs& a) {
 #pragma unroll
             for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int r = 0; r < W; ++r) v[u][r] = __ldcg(src[r] + i + u * stride);
+                for (int r = 0; r < W; ++r) v[u][r] = p2p_ld<LS>(src[r] + i + u * stride);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 float4 acc = v[u][0];
@@ -220,7 +234,7 @@ __device__ void average_shard(const SymmArgs& a) {
                 }
                 acc = scale4(acc, a.scale);
 #pragma unroll
-                for (int r = 0; r < W; ++r) __stcg(dst[r] + i + u * stride, acc);
+                for (int r = 0; r < W; ++r) p2p_st<LS>(dst[r] + i + u * stride, acc);
             }
         }
         for (; i < v1; i += stride) {
