@@ -114,7 +114,8 @@ __device__ int agreed_vote(const SymmArgs& s, uint64_t seq) {
 }
 
 template <bool MOM, bool NEST, int W>
-__device__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o, uint64_t seq) {
+__device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
+                                     uint64_t seq) {
     __shared__ unsigned long long s_ticket;
     __shared__ int s_vote;
     __shared__ bool s_last;
@@ -234,26 +235,24 @@ __device__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, co
     }
 }
 
+// update-first order: K13 over the whole buffer, vote exchange in the last
+// block, the mean as a device-side launch on sync (separate function so the
+// streaming loop keeps its registers)
 template <bool MOM, bool NEST, int W>
-__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o,
-                                                            Grids gr) {
+__device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
+                                     const Grids& gr, uint64_t seq) {
     __shared__ bool s_last;
-    const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
-    // the order of this step: identical on every rank (same decision history)
-    const bool norm_first = o.mode == 1 || (o.mode == 2 && *reinterpret_cast<volatile float*>(o.predictor) >= o.threshold);
-    uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {start, vote posted, votes in, -, last arrival, end}
-    if (mark && blockIdx.x == 0 && threadIdx.x == 0) mark[0] = now_ns();
-    if (norm_first) {
-        nf_body<MOM, NEST, W>(a, f, s, o, seq);
-        return;
-    }
+    uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;
     // ---- update first: K13 over the whole buffer, vote in the last block
     const double acc = sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
     Workspace ws = ws_view(f.ws);
     const double bsum = block_sum(acc);
     if (threadIdx.x == 0) {
         ws.partials[blockIdx.x] = bsum;
-        __threadfence_system();  // this block's parameter stores reach peers before the vote
+        // gpu scope suffices: the last block observes this counter and issues
+        // the system-scope fence before its release of the vote (causality is
+        // transitive), so peers reading after the vote see these stores
+        __threadfence();
         s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
@@ -281,6 +280,21 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
     } else {
         *s.seq = static_cast<uint32_t>(seq);
     }
+}
+
+template <bool MOM, bool NEST, int W>
+__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o,
+                                                            Grids gr) {
+    const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
+    // the order of this step: identical on every rank (same decision history)
+    const bool norm_first = o.mode == 1 || (o.mode == 2 && *reinterpret_cast<volatile float*>(o.predictor) >= o.threshold);
+    uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {start, vote posted, votes in, -, last arrival, end}
+    if (mark && blockIdx.x == 0 && threadIdx.x == 0) mark[0] = now_ns();
+    if (norm_first) {
+        nf_body<MOM, NEST, W>(a, f, s, o, seq);
+        return;
+    }
+    uf_body<MOM, NEST, W>(a, f, s, o, gr, seq);
 }
 
 // ------------------------------------------- gradient aggregation, one launch

@@ -6,8 +6,10 @@ mkdir -p gpurun_out
 if [ "$TEST" = "1" ]; then
 timeout 1200 python -m pytest tests/test_multigpu.py -x -q -k "symm or nan" > gpurun_out/pytest_mg_n$N.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_mg_n$N.log
 fi
-for OT in ${ORDERS:-"update_first 16384" "norm_first 8192" "norm_first 16384" "norm_first 32768" "adaptive 16384"}; do
-  set -- $OT
+# ORDERS: comma-separated "order:tile" pairs
+IFS=, read -ra PAIRS <<< "${ORDERS:-update_first:16384,norm_first:8192,norm_first:16384,norm_first:32768,adaptive:16384}"
+for OT in "${PAIRS[@]}"; do
+  set -- ${OT/:/ }
   timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29511 \
     bench.py --gpus $N --steps 100 --warmup 5 --order $1 --tile $2 --no-e2e > gpurun_out/bench_n${N}_$1_$2.json 2> gpurun_out/bench_n${N}_$1_$2.err
   echo "order $1 tile $2 rc=$?"
