@@ -205,9 +205,13 @@ class SelSyncStep:
         that path to one ctypes call."""
         from . import _native as N
 
-        key = (which, self.grads.data_ptr(), self.grads.numel())
-        if getattr(self, "_fast_key", None) != key:
-            # full validation whenever the bound gradient changes
+        g = self.grads
+        key = (which, g.data_ptr(), g.numel(), g.dtype, g.device, g.is_contiguous())
+        cache = self.__dict__.setdefault("_fast_cache", {})
+        entry = cache.get(key)
+        if entry is None:
+            # full validation whenever a gradient buffer is bound for the first
+            # time (a training loop may rotate a few buffers; each is checked once)
             K._sgd_check(self.params, self.grads, self.momentum, self.config.momentum)
             c = self.config
             m = self.momentum.data_ptr() if self.momentum is not None else None
@@ -216,15 +220,16 @@ class SelSyncStep:
             tail = [self.signal.state.data_ptr(), float(c.delta), self.signal.word.data_ptr(),
                     self.signal.trace.data_ptr(), self.signal.trace_capacity]
             if which in ("symm", "symm_ga"):
-                self._fast_fn = N.LIB.ss_step_symm_f32 if which == "symm" else N.LIB.ss_step_symm_ga_f32
+                fn = N.LIB.ss_step_symm_f32 if which == "symm" else N.LIB.ss_step_symm_ga_f32
                 tail += [self.symm.group_ref, self.ws.ptr]
             else:
-                self._fast_fn = N.LIB.ss_update_norm_signal_f32
+                fn = N.LIB.ss_update_norm_signal_f32
                 tail += [self.ws.ptr]
-            self._fast_parts = (head, hp, tail)
-            self._fast_key = key
-        head, hp, tail = self._fast_parts
-        rc = self._fast_fn(*head, lr, *hp, int(self.steps_done == 0), *tail, stream.cuda_stream)
+            if len(cache) >= 16:
+                cache.clear()
+            entry = cache[key] = (fn, head, hp, tail)
+        fn, head, hp, tail = entry
+        rc = fn(*head, lr, *hp, int(self.steps_done == 0), *tail, stream.cuda_stream)
         if rc:
             N.check(rc)
         K._count()
