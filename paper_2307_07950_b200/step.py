@@ -67,6 +67,7 @@ class SelSyncStep:
         order: str = "adaptive",
         order_threshold: float = 0.3,
         tile_elems: int = 16384,
+        multicast="auto",
     ):
         if not isinstance(config, SelSyncConfig):
             raise ConfigError("config must be a SelSyncConfig")
@@ -112,7 +113,7 @@ class SelSyncStep:
             self.symm = SymmetricParams(params.numel(), self.device, self.comm,
                                         ring_capacity=trace_capacity, timeout_s=timeout_s,
                                         order=order, order_threshold=order_threshold,
-                                        tile_elems=tile_elems)
+                                        tile_elems=tile_elems, use_multicast=multicast)
             if config.aggregation == "grads":
                 # the exchanged vector is the gradient: it lives in symmetric memory
                 self.symm.buf.copy_(grads)

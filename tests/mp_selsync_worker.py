@@ -70,7 +70,56 @@ def main():
     dist.destroy_process_group()
 
 
-if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "nan"):
+LARGE = dict(P=1_000_003, steps=14, seed=11, delta=0.05, warmup=2, smoothing=0.5, lr=0.05, momentum=0.9,
+             weight_decay=4e-4, tile=4096)  # decisions: 8 sync, 4 local, 2 sync (>= 4.7% from a tie)
+
+
+def large_init(seed, P):
+    """w0 ~ U(-0.05, 0.05) in fp32; rank 0's copy is broadcast."""
+    return np.random.default_rng(seed).uniform(-0.05, 0.05, P).astype(np.float32)
+
+
+def large_main():
+    """Many tiles and a ragged tail: P = 1,000,003 with 4096-element tiles
+    (245 tiles, lag groups, a 3-element scalar tail), momentum + weight decay,
+    mixed decisions; every step order / back end must give the oracle's trace."""
+    variant, out = sys.argv[2], Path(sys.argv[3])
+    opts = {"nccl": dict(collective="nccl", fuse=True),
+            "update_first": dict(collective="symm", flag_exchange="fused", order="update_first"),
+            "norm_first": dict(collective="symm", flag_exchange="fused", order="norm_first"),
+            "adaptive": dict(collective="symm", flag_exchange="fused", order="adaptive"),
+            "p2p-mean": dict(collective="symm", flag_exchange="fused", order="norm_first", multicast=False),
+            "nvls-mean": dict(collective="symm", flag_exchange="fused", order="adaptive", multicast=True),
+            "two-launch": dict(collective="symm", flag_exchange="p2p")}[variant]
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    c = LARGE
+    P = c["P"]
+    init = torch.from_numpy(large_init(c["seed"], P)).to(dev)
+    g = torch.zeros(P, device=dev)
+    cfg = SelSyncConfig(delta=c["delta"], warmup=c["warmup"], smoothing=c["smoothing"], momentum=c["momentum"],
+                        weight_decay=c["weight_decay"])
+    step = SelSyncStep(init, g, cfg, tile_elems=c["tile"], **opts)
+    for s in range(c["steps"]):
+        g.copy_(torch.from_numpy(O.synthetic_grad32(c["seed"], rank, s, P)), non_blocking=True)
+        if step.async_capable:
+            step.step_async(c["lr"])
+        else:
+            step.step(c["lr"])
+    step.synchronize()
+    recs = step.records()
+    np.savez(out / f"large_{variant}_rank{rank}.npz", decisions=np.array(step.decisions()),
+             ewma=np.array([r["ewma"] for r in recs]), params=step.params.double().cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "large":
+    large_main()
+elif __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "nan"):
     main()
 
 

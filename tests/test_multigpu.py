@@ -55,3 +55,51 @@ def test_nan_on_one_rank_raises_everywhere(tmp_path):
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     for r in range(2):
         assert bool(np.load(tmp_path / f"nan_rank{r}.npz")["raised"])
+
+
+@pytest.fixture(scope="module")
+def large_oracle():
+    """Oracle run of mp_selsync_worker.LARGE per world size (float64 numpy)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import mp_selsync_worker as MW
+    from oracle import selsync_oracle as O
+
+    c = MW.LARGE
+    cache = {}
+
+    def get(n):
+        if n not in cache:
+            init = MW.large_init(c["seed"], c["P"]).astype(np.float64)
+            cache[n] = O.simulate_selsync(
+                init, n, c["steps"], lambda w, s, _p: O.synthetic_grad32(c["seed"], w, s, c["P"]).astype(np.float64),
+                delta=c["delta"], warmup=c["warmup"], smoothing=c["smoothing"], lr=c["lr"], momentum=c["momentum"],
+                weight_decay=c["weight_decay"])
+        return cache[n]
+    return get
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("variant", ["nccl", "update_first", "norm_first", "adaptive", "p2p-mean", "nvls-mean",
+                                     "two-launch"])
+def test_large_ragged_many_tiles_match_oracle(n, variant, tmp_path, large_oracle):
+    """P = 1,000,003 in 4096-element tiles, momentum + weight decay, mixed
+    decisions: the tile tickets, lag groups, scalar tail and every back end
+    against the float64 oracle (decisions exact but for ties, params 1e-5)."""
+    if NGPU < n:
+        pytest.skip(f"needs {n} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", "--master-port=29535",
+           str(ROOT / "tests" / "mp_selsync_worker.py"), "large", variant, str(tmp_path)]
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+    import mp_selsync_worker as MW
+
+    ref = large_oracle(n)
+    for rank in range(n):
+        z = np.load(tmp_path / f"large_{variant}_rank{rank}.npz")
+        assert_trace_parity(z["decisions"], ref.decision, ref.delta_g, MW.LARGE["delta"], MW.LARGE["warmup"])
+        np.testing.assert_allclose(z["ewma"], ref.ewma[:, rank], rtol=1e-5)
+        params_close(z["params"], ref.finals[rank])
+    assert 0 < int(np.sum(z["decisions"][MW.LARGE["warmup"]:])) < MW.LARGE["steps"] - MW.LARGE["warmup"], \
+        "case must mix sync and local steps"
