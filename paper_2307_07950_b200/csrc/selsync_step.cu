@@ -154,13 +154,19 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
         }
     }
     __syncthreads();
-    // ---- phase 2: tickets -- groups of N update tiles + 1 mean of an owned tile
+    // ---- phase 2: tickets -- groups of N update tiles + 1 mean of an owned tile.
+    //      The next ticket is fetched while this one is worked on (its atomic
+    //      latency hides behind the tile); a block still takes its tickets in
+    //      increasing order, so tickets only ever wait on earlier ones.
+    unsigned long long nxt = 0;
+    if (threadIdx.x == 0) nxt = atomicAdd(o.ticket, 1ull);
     for (;;) {
-        if (threadIdx.x == 0) s_ticket = atomicAdd(o.ticket, 1ull);
+        if (threadIdx.x == 0) s_ticket = nxt;
         __syncthreads();
         const unsigned long long k = s_ticket;
         __syncthreads();
         if (k >= total) break;
+        if (threadIdx.x == 0) nxt = atomicAdd(o.ticket, 1ull);
         const bool rec = o.dbg != nullptr && static_cast<int64_t>(k) < o.dbg_cap && threadIdx.x == 0;
         uint64_t t_start = rec ? now_ns() : 0, t_ready = 0;
         int64_t rec_tile = -1;
@@ -176,10 +182,9 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                     const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
                     sgd_block_range<MOM, NEST>(a, e0, e1);
                     __syncthreads();
-                    if (threadIdx.x == 0) {
-                        __threadfence_system();
-                        red_add_release_sys(o.cnt[t % N] + t, 1u);
-                    }
+                    // release at sys scope: the block's stores (ordered by the
+                    // barrier) are visible to the owner before the count
+                    if (threadIdx.x == 0) red_add_release_sys(o.cnt[t % N] + t, 1u);
                     rec_tile = t;
                 }
             } else {
@@ -348,12 +353,15 @@ __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish 
     if (threadIdx.x == 0) s_vote = agreed_vote(s, seq);
     __syncthreads();
     const bool sync = s_vote == SS_FLAG_SYNC;
+    unsigned long long nxt = 0;  // next ticket fetched ahead, as in nf_body
+    if (threadIdx.x == 0) nxt = atomicAdd(o.ticket, 1ull);
     for (;;) {
-        if (threadIdx.x == 0) s_ticket = atomicAdd(o.ticket, 1ull);
+        if (threadIdx.x == 0) s_ticket = nxt;
         __syncthreads();
         const unsigned long long k = s_ticket;
         __syncthreads();
         if (k >= total) break;
+        if (threadIdx.x == 0) nxt = atomicAdd(o.ticket, 1ull);
         const int64_t grp = static_cast<int64_t>(k / (N + 1));
         const int pos = static_cast<int>(k % (N + 1));
         if (pos == 0) {
@@ -363,10 +371,8 @@ __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish 
                 const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
                 average_block_range<W>(s, e0, e1);
                 __syncthreads();
-                if (threadIdx.x == 0) {
-                    __threadfence_system();
+                if (threadIdx.x == 0)
                     for (int j = 0; j < N; ++j) red_add_release_sys(o.cnt[j] + t, 1u);
-                }
             }
         } else {
             // ---- update tile t of group grp - lag (owner t % N), with the mean gradient on sync

@@ -79,6 +79,10 @@ def large_init(seed, P):
     return np.random.default_rng(seed).uniform(-0.05, 0.05, P).astype(np.float32)
 
 
+def large_aggregation(variant):
+    return "grads" if variant.startswith("ga") else "params"
+
+
 def large_main():
     """Many tiles and a ragged tail: P = 1,000,003 with 4096-element tiles
     (245 tiles, lag groups, a 3-element scalar tail), momentum + weight decay,
@@ -90,7 +94,9 @@ def large_main():
             "adaptive": dict(collective="symm", flag_exchange="fused", order="adaptive"),
             "p2p-mean": dict(collective="symm", flag_exchange="fused", order="norm_first", multicast=False),
             "nvls-mean": dict(collective="symm", flag_exchange="fused", order="adaptive", multicast=True),
-            "two-launch": dict(collective="symm", flag_exchange="p2p")}[variant]
+            "two-launch": dict(collective="symm", flag_exchange="p2p"),
+            "ga": dict(collective="symm", flag_exchange="fused"),
+            "ga-nccl": dict(collective="nccl", fuse=True)}[variant]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -101,8 +107,9 @@ def large_main():
     init = torch.from_numpy(large_init(c["seed"], P)).to(dev)
     g = torch.zeros(P, device=dev)
     cfg = SelSyncConfig(delta=c["delta"], warmup=c["warmup"], smoothing=c["smoothing"], momentum=c["momentum"],
-                        weight_decay=c["weight_decay"])
+                        weight_decay=c["weight_decay"], aggregation=large_aggregation(variant))
     step = SelSyncStep(init, g, cfg, tile_elems=c["tile"], **opts)
+    g = step.grads  # gradient aggregation over symmetric memory owns the gradient buffer
     for s in range(c["steps"]):
         g.copy_(torch.from_numpy(O.synthetic_grad32(c["seed"], rank, s, P)), non_blocking=True)
         if step.async_capable:
