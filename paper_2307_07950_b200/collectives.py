@@ -109,7 +109,7 @@ class SymmetricParams:
 
     def __init__(self, numel: int, device, comm: RankGroup, *, ring_capacity: int = 1 << 14,
                  timeout_s: float = 30.0, use_multicast="auto", order: str = "update_first",
-                 order_threshold: float = 0.3, tile_elems: int = 16384):
+                 order_threshold: float = 0.2, tile_elems: int = 16384):
         import ctypes
 
         import torch.distributed._symmetric_memory as symm_mem

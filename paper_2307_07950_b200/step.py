@@ -65,7 +65,7 @@ class SelSyncStep:
         profile: bool = False,
         timeout_s: float = 10.0,
         order: str = "adaptive",
-        order_threshold: float = 0.3,
+        order_threshold: float = 0.2,
         tile_elems: int = 16384,
         multicast="auto",
     ):
