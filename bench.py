@@ -334,21 +334,28 @@ def main():
 
     clocks = ClockSampler(local)
     # ---- headline: 50% sync mix, device-resident inputs
-    mixed = make_step(0.3)
-    run(mixed, args.warmup)
+    failure = None
     if world > 1 and args.collective == "symm":
-        # safety net: if the device-side exchange ever times out on this box,
-        # measure the NCCL back end instead of hanging the run
+        # safety net: if symmetric memory cannot be set up or the device-side
+        # exchange times out on this box, ALL ranks agree to measure the NCCL
+        # back end instead of hanging or dying
         from paper_2307_07950_b200.errors import TransportError
 
         try:
+            mixed = make_step(0.3)
+            run(mixed, args.warmup)
             mixed.synchronize()
-        except TransportError as exc:
-            print(f"bench: symmetric-memory exchange failed ({exc}); falling back to NCCL",
+        except (TransportError, RuntimeError) as exc:
+            failure = exc
+        if comm.max_float(1.0 if failure is not None else 0.0, dev) > 0.0:
+            print(f"bench: symmetric-memory path failed on some rank ({failure}); falling back to NCCL",
                   file=sys.stderr, flush=True)
             args.collective = "nccl"
             mixed = make_step(0.3)
             run(mixed, args.warmup)
+    else:
+        mixed = make_step(0.3)
+        run(mixed, args.warmup)
     clocks.start()
     res = timed(mixed, args.steps)
     clocks.stop()
