@@ -56,7 +56,8 @@ def parse():
                          "workloads add stock PyTorch fwd/bwd of BASELINE configs 1-3")
     ap.add_argument("--delta", type=float, default=0.3, help="delta for model workloads")
     ap.add_argument("--graph", action="store_true",
-                    help="model workloads: capture fwd + bwd + SelSync step in one CUDA graph")
+                    help="model workloads: capture fwd + bwd + SelSync step in one CUDA graph; microbench: "
+                         "replay one captured step per gradient buffer (launch-bound small P)")
     ap.add_argument("--sel-warmup", type=int, default=25, help="EWMA window / warmup for model workloads")
     ap.add_argument("--momentum", type=float, default=0.9)
     ap.add_argument("--weight-decay", type=float, default=4e-4)
@@ -239,7 +240,12 @@ def workload_config(args, world):
                         + ("NVLink symmetric memory" if args.collective == "symm" else "NCCL") + ")"
                         if world > 1 else "dp1 (single replica, no exchange)"),
         "value_counts": "worker-steps: N ranks x K steps / (max-over-ranks device time)",
-        "l2": f"inputs exceed L2: w, g, m = {12 * args.P / 1e9:.2f} GB per step vs 126 MB L2",
+        "l2": (f"inputs exceed L2: w, g, m = {12 * args.P / 1e9:.2f} GB per step vs 126 MB L2"
+               if 12 * args.P > 126e6 else
+               f"inputs fit in L2 ({12 * args.P / 1e6:.1f} MB, not flushed): a small-P sweep point, "
+               "launch/latency-bound, not a bandwidth claim"),
+        "launch": ("one CUDA graph replay per step (captured per gradient buffer)" if args.graph
+                   else "one host launch per step"),
     }
 
 
@@ -289,8 +295,10 @@ def main():
         st = SelSyncStep(w, g, cfg, momentum_buffer=mom, group=comm, fuse=not args.no_fuse,
                          collective=args.collective if world > 1 else None,
                          flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
-                         trace_capacity=1 << 14, profile=True, order=args.order, tile_elems=args.tile)
+                         trace_capacity=1 << 14, profile=not args.graph, order=args.order, tile_elems=args.tile)
         return st
+
+    captured = {}  # --graph: one CUDA graph per (step object, gradient buffer)
 
     def run(step, n, host_ring=None, host_row=None):
         """n steps. Device-resident inputs: step_async (no host round-trip) when
@@ -304,6 +312,12 @@ def main():
                 step.step(args.lr)
                 host_row.copy_(step.signal.trace[:32], non_blocking=True)
                 torch.cuda.current_stream().synchronize()
+            elif args.graph and step.async_capable and step.steps_done > 0:
+                graphs = captured.setdefault(id(step), {})
+                if k not in graphs:
+                    step.grads = grads_ring[k]
+                    graphs[k] = step.capture(args.lr)
+                graphs[k].replay()
             else:
                 step.grads = grads_ring[k]  # bind this step's resident gradient
                 if step.async_capable:
@@ -414,6 +428,10 @@ def main():
     # roofline of the update kernel: its per-launch time on local steps (at
     # N > 1 with the one-launch step this also holds the vote exchange)
     kms = sorted(modes["all_local"]["kernel_ms"])
+    timed_on = "all_local mode, CUDA events around every launch on the launching stream"
+    if not kms:  # --graph: no events inside graphs; bound the kernel by the whole local step
+        kms = [modes["all_local"]["ms"] / args.steps]
+        timed_on = "all_local step time under graph replay (upper bound of the kernel time)"
     k_mean = sum(kms) / len(kms)
     bytes_per_launch = (20 if args.momentum else 12) * P
     if args.no_fuse:
@@ -455,7 +473,7 @@ def main():
             "kernel_ms_mean": k_mean,
             "kernel_ms_median": kms[len(kms) // 2],
             "kernel_share_of_local_step": k_mean / (modes["all_local"]["ms"] / args.steps),
-            "timed_on": "all_local mode, CUDA events around every launch on the launching stream",
+            "timed_on": timed_on,
         },
         "gpu_launches": res["launches"],
         "clocks": clocks.summary(),
@@ -463,7 +481,7 @@ def main():
     }
     for name, m in modes.items():
         ent = {"steps_per_s": world * args.steps / (m["ms"] / 1e3), "ms_per_step": m["ms"] / args.steps,
-               "kernel_ms_mean": sum(m["kernel_ms"]) / len(m["kernel_ms"])}
+               "kernel_ms_mean": sum(m["kernel_ms"]) / len(m["kernel_ms"]) if m["kernel_ms"] else None}
         ent.update(exchange_stats(m, P, world))
         line["modes"][name] = ent
     line.update({"exchange": exchange_stats(res, P, world)} if world > 1 else {})

@@ -304,6 +304,26 @@ class SelSyncStep:
         self.lrs.append(lr)
         return "sync" if synced else "local"
 
+    def capture(self, lr: float) -> "CapturedStep":
+        """Record one device-branching step (the gradient buffer bound now, this
+        lr) as a CUDA graph; ``replay()`` then equals ``step_async(lr)`` at the
+        cost of one graph launch. For launch-bound sizes (small P) and loops
+        that rotate a fixed set of gradient buffers (capture one per buffer)."""
+        if not self.async_capable:
+            raise ConfigError("capture needs a device-side branch (collective='symm' or a single rank)")
+        if self.profile:
+            raise ConfigError("per-launch profiling events cannot be captured")
+        if self.steps_done == 0:
+            raise ConfigError("run one eager step first (the first step initialises the momentum buffer)")
+        lr = self._check_lr(lr)
+        stream = torch.cuda.current_stream(self.device)
+        torch.cuda.synchronize(self.device)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self._enqueue_device_step(lr, torch.cuda.current_stream(self.device))
+        stream.synchronize()
+        return CapturedStep(self, graph, lr)
+
     # ------------------------------------------------------------------
     def synchronize(self) -> None:
         """Wait for enqueued steps; raise on device-side errors (NaN norm, peer timeout)."""
@@ -375,6 +395,19 @@ class SelSyncStep:
 
     def sync_ms(self) -> list[float]:
         return [a.elapsed_time(b) for a, b in self.sync_events]
+
+
+class CapturedStep:
+    """A SelSync step recorded as a CUDA graph (``SelSyncStep.capture``)."""
+
+    def __init__(self, step: SelSyncStep, graph, lr: float):
+        self.step, self.graph, self.lr = step, graph, lr
+
+    def replay(self) -> None:
+        self.graph.replay()
+        self.step.steps_done += 1
+        self.step.lrs.append(self.lr)
+        K._count()
 
 
 class TensorListSelSyncStep:

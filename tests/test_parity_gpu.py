@@ -23,7 +23,7 @@ pytestmark = pytest.mark.gpu
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from paper_2307_07950_b200 import SelSyncConfig, SignalError  # noqa: E402
+from paper_2307_07950_b200 import ConfigError, SelSyncConfig, SignalError  # noqa: E402
 from paper_2307_07950_b200.replicas import ReplicaSelSync  # noqa: E402
 from paper_2307_07950_b200.step import SelSyncStep  # noqa: E402
 
@@ -147,6 +147,35 @@ def test_single_rank_async_steps_match_oracle():
     assert len(got) == 64
     assert_trace_parity(got, ref.decision[-64:], ref.delta_g[-64:], delta, -1)
     params_close(w.double().cpu().numpy(), ref.finals[0])
+
+
+def test_captured_steps_match_oracle():
+    """SelSyncStep.capture: one CUDA graph per gradient buffer, replayed --
+    the same trace and parameters as the oracle (and as eager steps)."""
+    d, steps, seed, delta, warmup, lr = 3000, 40, 17, 0.003, 2, 0.1
+    P = 2 * d + 2
+    init = O.init_params_linear(d, 5).astype(np.float32).astype(np.float64)
+    w = torch.tensor(init, dtype=torch.float32, device=DEV)
+    bufs = [torch.zeros_like(w) for _ in range(steps)]
+    for s in range(steps):
+        bufs[s].copy_(torch.from_numpy(O.synthetic_grad32(seed, 0, s, P)))
+    step = SelSyncStep(w, bufs[0], SelSyncConfig(delta=delta, warmup=warmup, momentum=0.9, weight_decay=4e-4))
+    step.step_async(lr)  # the first step initialises the momentum buffer eagerly
+    graphs = []
+    for s in range(1, steps):
+        step.grads = bufs[s]
+        graphs.append(step.capture(lr))
+    assert step.steps_done == 1  # capturing does not run a step
+    for gr in graphs:
+        gr.replay()
+    step.synchronize()
+    ref = O.simulate_selsync(init, 1, steps, lambda w_, s, _p: O.synthetic_grad32(seed, 0, s, P),
+                             delta=delta, warmup=warmup, lr=lr, momentum=0.9, weight_decay=4e-4)
+    assert 0 < ref.decision.sum() < steps
+    assert_trace_parity(step.decisions(), ref.decision, ref.delta_g, delta, warmup)
+    params_close(w.double().cpu().numpy(), ref.finals[0])
+    with pytest.raises(ConfigError):
+        SelSyncStep(w.clone(), bufs[0], SelSyncConfig(delta=delta, warmup=warmup)).capture(lr)
 
 
 def test_nan_gradient_raises_signal_error():

@@ -1,22 +1,34 @@
 #!/bin/bash
-# BASELINE configs[4]: flattened parameter sweep, N = 1 and N = 2 (one box)
+# BASELINE configs[4]: flattened parameter sweep 1M-1B, forced all-local / all-sync
+# and the 50% mix, at N in $NS (default "1 2 4"). P <= 16M replays one CUDA graph
+# per step (launch-bound sizes); larger P uses the host launch path with events.
+NS=${NS:-"1 2 4"}
+SIZES=${SIZES:-"1000000 4000000 16000000 64000000 100000000 256000000 1000000000"}
 mkdir -p gpurun_out/sweep
-for P in 1000000 16000000 100000000 1000000000; do
-  python bench.py --P $P --steps 50 --warmup 5 --no-e2e --no-cpu-baseline > gpurun_out/sweep/n1_$P.json 2>/dev/null
-  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29521 \
-    bench.py --gpus 2 --P $P --steps 50 --warmup 5 --no-e2e > gpurun_out/sweep/n2_$P.json 2>/dev/null
-  python - $P <<'PY'
+for P in $SIZES; do
+  G=""; [ "$P" -le 16000000 ] && G="--graph"
+  for N in $NS; do
+    if [ "$N" = "1" ]; then
+      timeout 600 python bench.py --P $P --steps 50 --warmup 5 --no-e2e --no-cpu-baseline $G \
+        > gpurun_out/sweep/n1_$P.json 2> gpurun_out/sweep/n1_$P.err
+    else
+      timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+        --master-port 2952$N bench.py --gpus $N --P $P --steps 50 --warmup 5 --no-e2e $G \
+        > gpurun_out/sweep/n${N}_$P.json 2> gpurun_out/sweep/n${N}_$P.err
+    fi
+  done
+  python - $P "$NS" <<'PY'
 import json, sys
 P = int(sys.argv[1])
-for n in (1, 2):
+for n in sys.argv[2].split():
     try:
         d = json.loads(open(f"gpurun_out/sweep/n{n}_{P}.json").read().strip().splitlines()[-1])
     except Exception as e:
         print(P, n, "fail", e); continue
     m = d["modes"]
     ex = d.get("exchange", {}).get("nvlink", {})
-    print(f"P={P:>11,} N={n}: mixed {d['value']:9.1f} steps/s  local {m['all_local']['ms_per_step']*1e3:8.1f} us  "
+    print(f"P={P:>13,} N={n}: mixed {d['value']:9.1f} steps/s  local {m['all_local']['ms_per_step']*1e3:8.1f} us  "
           f"sync {m['all_sync']['ms_per_step']*1e3:8.1f} us  K13 {d['roofline']['achieved']:6.0f} GB/s ({d['roofline']['frac']:.3f})  "
-          f"C2 busbw {ex.get('busbw', float('nan')):6.0f}")
+          f"C2 busbw {ex.get('busbw', float('nan')):6.0f}  {d['config'].get('launch', '')[:9]}")
 PY
 done
