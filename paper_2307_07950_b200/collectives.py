@@ -116,7 +116,7 @@ class SymmetricParams:
 
         from . import _native as N
 
-        if comm.group is None and not comm.distributed:
+        if not dist.is_initialized():
             raise ConfigError("symmetric memory needs an initialised process group")
         self.device = torch.device(device)
         self.comm = comm
@@ -204,8 +204,8 @@ class SymmetricParams:
 
     @property
     def one_launch_capable(self) -> bool:
-        """The fused one-launch step supports NVLS or P2P widths 2, 4, 8."""
-        return self.multicast or self.world in (2, 4, 8)
+        """The fused one-launch step supports NVLS or P2P widths 1, 2, 4, 8."""
+        return self.multicast or self.world in (1, 2, 4, 8)
 
     def check(self) -> None:
         if int(self.err.item()) != 0:

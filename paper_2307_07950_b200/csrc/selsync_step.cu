@@ -516,11 +516,12 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
     const bool mom = momentum != 0.0f, nest = nesterov != 0;
     switch (symm_width(sa)) {
         case 0: return dispatch_step<0>(a, f, sa, o, mom, nest, stream);
+        case 1: return dispatch_step<1>(a, f, sa, o, mom, nest, stream);  // single rank (profiling)
         case 2: return dispatch_step<2>(a, f, sa, o, mom, nest, stream);
         case 4: return dispatch_step<4>(a, f, sa, o, mom, nest, stream);
         case 8: return dispatch_step<8>(a, f, sa, o, mom, nest, stream);
         default:
-            return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 2, 4, 8)", sa.world);
+            return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 1, 2, 4, 8)", sa.world);
     }
 }
 
@@ -562,10 +563,11 @@ extern "C" int ss_step_symm_ga_f32(float* w, float* g, float* m, int64_t n, floa
     const bool mom = momentum != 0.0f, nest = nesterov != 0;
     switch (symm_width(sa)) {
         case 0: return dispatch_step_ga<0>(a, f, sa, o, mom, nest, stream);
+        case 1: return dispatch_step_ga<1>(a, f, sa, o, mom, nest, stream);
         case 2: return dispatch_step_ga<2>(a, f, sa, o, mom, nest, stream);
         case 4: return dispatch_step_ga<4>(a, f, sa, o, mom, nest, stream);
         case 8: return dispatch_step_ga<8>(a, f, sa, o, mom, nest, stream);
         default:
-            return fail(SS_ERR_CONFIG, "gradient aggregation: world %d needs multicast (P2P widths 2, 4, 8)", sa.world);
+            return fail(SS_ERR_CONFIG, "gradient aggregation: world %d needs multicast (P2P widths 1, 2, 4, 8)", sa.world);
     }
 }

@@ -92,7 +92,10 @@ class SelSyncStep:
             raise ConfigError(f"flag_exchange must be 'fused', 'p2p' or 'nccl', got {flag_exchange!r}")
         if flag_exchange in ("p2p", "fused") and collective != "symm" and self.world > 1:
             raise ConfigError("the P2P flag exchange runs inside the symmetric-memory kernels")
-        self.collective = collective if self.world > 1 else "none"
+        # one rank: no exchange -- unless symmetric memory is asked for explicitly
+        # (the one-launch kernel on a single GPU, e.g. to profile it under ncu)
+        self.collective = collective if (self.world > 1 or collective == "symm"
+                                        and torch.distributed.is_initialized()) else "none"
         self.flag_exchange = flag_exchange
         self.fuse = (bool(fuse) or self.collective == "symm") and config.aggregation == "params"
         if self.collective == "symm" and config.aggregation == "grads" and flag_exchange != "fused":

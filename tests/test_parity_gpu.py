@@ -178,6 +178,37 @@ def test_captured_steps_match_oracle():
         SelSyncStep(w.clone(), bufs[0], SelSyncConfig(delta=delta, warmup=warmup)).capture(lr)
 
 
+@pytest.mark.parametrize("order", ["update_first", "norm_first", "adaptive"])
+def test_single_rank_symmetric_step_matches_oracle(order, tmp_path):
+    """The one-launch symmetric-memory step on one rank (world-1 group, the
+    configuration used to profile it under ncu): same trace and parameters."""
+    import torch.distributed as dist
+
+    d, steps, seed, delta, warmup, lr = 40000, 24, 23, 0.03, 2, 0.1  # 8 local, 16 sync (4.7% from a tie)
+    P = 2 * d + 2
+    init = O.init_params_linear(d, 6).astype(np.float32).astype(np.float64)
+    dist.init_process_group("nccl", init_method=f"file://{tmp_path}/pg", rank=0, world_size=1, device_id=DEV)
+    try:
+        w = torch.tensor(init, dtype=torch.float32, device=DEV)
+        g = torch.zeros_like(w)
+        step = SelSyncStep(w, g, SelSyncConfig(delta=delta, warmup=warmup, momentum=0.9, weight_decay=4e-4),
+                           collective="symm", order=order, tile_elems=4096)
+        assert step.collective == "symm" and step.flag_exchange == "fused"
+        for s in range(steps):
+            g.copy_(torch.from_numpy(O.synthetic_grad32(seed, 0, s, P)))
+            step.step_async(lr)
+        step.synchronize()
+        got_w = step.params.double().cpu().numpy()
+        got_dec = step.decisions()
+    finally:
+        dist.destroy_process_group()
+    ref = O.simulate_selsync(init, 1, steps, lambda w_, s, _p: O.synthetic_grad32(seed, 0, s, P),
+                             delta=delta, warmup=warmup, lr=lr, momentum=0.9, weight_decay=4e-4)
+    assert 0 < ref.decision.sum() < steps
+    assert_trace_parity(got_dec, ref.decision, ref.delta_g, delta, warmup)
+    params_close(got_w, ref.finals[0])
+
+
 def test_nan_gradient_raises_signal_error():
     w = torch.zeros(1000, device=DEV)
     g = torch.ones_like(w)
