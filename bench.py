@@ -67,7 +67,8 @@ def parse():
                     help="C2 back end at N > 1: device-conditional symmetric-memory kernel or host-branch NCCL")
     ap.add_argument("--flag-exchange", default="fused", choices=["fused", "p2p", "nccl"],
                     help="fused: the whole step in one cooperative launch (symm only)")
-    ap.add_argument("--tile", type=int, default=16384, help="elements per tile of the overlapped sync step")
+    ap.add_argument("--tile", type=int, default=None,
+                    help="elements per tile of the overlapped sync step (default: 4096 up to 2M params, else 16384)")
     ap.add_argument("--order", default="adaptive", choices=["update_first", "norm_first", "adaptive"],
                     help="one-launch step order (flag-exchange fused): norm_first overlaps update and mean")
     ap.add_argument("--no-cpu-baseline", action="store_true")

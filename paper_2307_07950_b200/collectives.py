@@ -109,7 +109,7 @@ class SymmetricParams:
 
     def __init__(self, numel: int, device, comm: RankGroup, *, ring_capacity: int = 1 << 14,
                  timeout_s: float = 30.0, use_multicast="auto", order: str = "update_first",
-                 order_threshold: float = 0.2, tile_elems: int = 16384):
+                 order_threshold: float = 0.2, tile_elems: Optional[int] = None):
         import ctypes
 
         import torch.distributed._symmetric_memory as symm_mem
@@ -162,6 +162,10 @@ class SymmetricParams:
         # with the mean on sync steps and needs per-tile arrival counters
         if order not in self.ORDERS:
             raise ConfigError(f"order must be one of {sorted(self.ORDERS)}, got {order!r}")
+        if tile_elems is None:
+            # measured (N = 2, one graph replay per step): 4096-element tiles win
+            # below ~2M parameters (more tiles than blocks), 16384 from 4M up
+            tile_elems = 4096 if numel <= (1 << 21) else 16384
         if tile_elems <= 0 or tile_elems % 4:
             raise ConfigError("tile_elems must be a positive multiple of 4")
         self.order = order

@@ -66,7 +66,7 @@ class SelSyncStep:
         timeout_s: float = 10.0,
         order: str = "adaptive",
         order_threshold: float = 0.2,
-        tile_elems: int = 16384,
+        tile_elems: Optional[int] = None,
         multicast="auto",
     ):
         if not isinstance(config, SelSyncConfig):
