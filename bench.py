@@ -329,7 +329,7 @@ def main():
     def timed(step, n, **kw):
         comm.barrier(dev)
         torch.cuda.synchronize()
-        launches0 = K.LAUNCHES + device_launches(step)
+        launches0 = K.LAUNCHES
         k0 = len(step.kernel_events)
         s0 = len(step.sync_events)
         d0 = step.steps_done
@@ -345,7 +345,7 @@ def main():
         sms = step.sync_ms()[s0:]
         dec = step.decisions()[d0 - step.steps_done:]
         return dict(ms=ms, decisions=dec, kernel_ms=kms, sync_ms=sms,
-                    launches=K.LAUNCHES + device_launches(step) - launches0)
+                    launches=K.LAUNCHES - launches0)
 
     clocks = ClockSampler(local)
     # ---- headline: 50% sync mix, device-resident inputs
@@ -550,7 +550,6 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
     comm.barrier(dev)
     ms = comm.max_float(a.elapsed_time(b), dev)
     launches = K.LAUNCHES - l0 if not graph else args.steps  # one SelSync kernel per replayed graph
-    launches += device_launches(st)
     kms = st.kernel_ms()[k0:]
     dec = st.decisions()[d0 - st.steps_done:]
     # roofline of the update launch on local steps (sync steps add the mean)
@@ -610,12 +609,6 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
     if world > 1:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
-
-
-def device_launches(step) -> int:
-    """Kernels our step kernel launched from the device (CUDA dynamic parallelism)."""
-    sp = getattr(step, "symm", None)
-    return 0 if sp is None else int(sp.child_launches.item())
 
 
 def exchange_stats(m, P, world):

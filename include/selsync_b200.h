@@ -220,7 +220,7 @@ typedef struct ss_symm_group {
     float* predictor;                   /* EWMA of agreed sync decisions (zeroed) */
     int64_t tile_elems;                 /* elements per tile, multiple of 4 */
     int64_t n_tiles;                    /* capacity of every tile_cnt array */
-    uint32_t* child_launches;           /* optional: +1 per device-side (tail) launch */
+    void* reserved0;                    /* unused (layout slot), pass NULL */
     uint64_t* debug_events;             /* optional: per-ticket timeline of the overlapped step */
     int64_t debug_cap;                  /* tickets recorded (4 x uint64 each) */
 } ss_symm_group;

@@ -31,9 +31,8 @@ FLAGS = [
     "-Xptxas",
     "-v",
     "--expt-relaxed-constexpr",
-    "-rdc=true",  # CUDA dynamic parallelism: the step kernel tail-launches the NVLink mean
 ]
-LIBS = ["-lcudadevrt"]
+LIBS: list[str] = []
 
 
 def nvcc() -> str:

@@ -86,7 +86,7 @@ class SymmGroupC(Structure):
         ("predictor", c_void_p),
         ("tile_elems", c_int64),
         ("n_tiles", c_int64),
-        ("child_launches", c_void_p),
+        ("reserved0", c_void_p),
         ("debug_events", c_void_p),
         ("debug_cap", c_int64),
     ]

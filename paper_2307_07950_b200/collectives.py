@@ -183,8 +183,6 @@ class SymmetricParams:
         g.predictor = self.predictor.data_ptr()
         g.tile_elems = int(tile_elems)
         g.n_tiles = int(self.n_tiles)
-        self.child_launches = torch.zeros(1, dtype=torch.int32, device=self.device)
-        g.child_launches = self.child_launches.data_ptr()
 
         self.group_c = g
         self.group_ref = ctypes.byref(g)
@@ -200,7 +198,7 @@ class SymmetricParams:
     def enable_timeline(self, capacity: int) -> torch.Tensor:
         """Record the per-ticket timeline of the overlapped sync step (tooling):
         4 x int64 per ticket {kind << 48 | tile, t_start, t_ready, t_end} (ns)."""
-        # + 8 markers: step start, last arrival, votes in, child launched, last arrival, barrier done
+        # + 8 markers: step start, vote posted, votes in, -, last arrival, barrier done
         self.timeline = torch.zeros(4 * int(capacity) + 8, dtype=torch.int64, device=self.device)
         self.group_c.debug_events = self.timeline.data_ptr()
         self.group_c.debug_cap = int(capacity)

@@ -34,6 +34,9 @@ __host__ __device__ inline Workspace ws_view(void* ws) {
     char* b = static_cast<char*>(ws);
     return Workspace{reinterpret_cast<unsigned int*>(b), reinterpret_cast<double*>(b + kWsHeader)};
 }
+// header: norm arrival counter at 0, exchange arrival counter at 64, ticket at
+// 128, the update-first step's decision broadcast at 192; then the partials
+constexpr int64_t kWsBytes = kWsHeader + 8 * kMaxGrid;
 
 // ------------------------------------------- exact IEEE scalar arithmetic
 // The signal math must round exactly like the reference's Python floats:

@@ -281,7 +281,7 @@ int ss_decide(const ss_signal_state* st, double delta, int32_t* sync_out) {
 
 int ss_workspace_bytes(int64_t* bytes) {
     if (!bytes) return fail(SS_ERR_CONFIG, "null output");
-    *bytes = kWsHeader + static_cast<int64_t>(sizeof(double)) * kMaxGrid;
+    *bytes = kWsBytes;
     return SS_OK;
 }
 

@@ -9,14 +9,13 @@
 //
 //  update first (order 0): K13 -- update + ||g||^2 over the whole buffer; the
 //     last block to arrive reduces the partials, runs K2, posts its vote to
-//     every peer's signal slot and waits for the N votes (C1: MAX = OR); every
-//     other block has already exited. On sync it tail-launches avg_kernel
-//     (CUDA dynamic parallelism, cudaStreamTailLaunch) -- the NVLink mean of
-//     this rank's shard with the 1/N in the epilogue (C2) + end barrier.
+//     every peer's signal slot and waits for the N votes (C1: MAX = OR), then
+//     broadcasts the agreed word to the other blocks of the (one-wave) grid.
+//     On sync all blocks run the NVLink mean of this rank's shard with the 1/N
+//     in the epilogue (C2) + end barrier; on local steps they exit.
 //     20P HBM bytes; a sync step pays update + mean back to back.
 //
-//  norm first (order 1): ONE ticketed pass of the same launch, no device-side
-//     launch: first the ||g||^2 tiles (4P; the block that finishes the last
+//  norm first (order 1): ONE ticketed pass of the same launch: first the ||g||^2 tiles (4P; the block that finishes the last
 //     one runs K2 and posts the vote), then groups of N update tiles and one
 //     mean ticket for a tile this rank owns (tile t belongs to rank t mod N)
 //     that was updated `lag` groups earlier. A rank announces a finished
@@ -56,15 +55,8 @@ struct OverlapArgs {
     int64_t n_tiles;
     int lag;                   // groups between an update ticket and the owner's mean ticket
     unsigned long long* ticket;
-    uint32_t* child_launches;  // optional launch counter (device-side launches)
     uint64_t* dbg;             // optional per-ticket timeline: {kind << 48 | tile, t0, t_ready, t_end}
     int64_t dbg_cap;
-};
-
-struct Grids {
-    int avg;   // avg_kernel
-    int upd;   // plain update (order 1, local steps)
-    int ua;    // upd_avg_kernel
 };
 
 __device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
@@ -83,18 +75,6 @@ __device__ void end_barrier(const SymmArgs& s, uint64_t seq) {
     bool to = false;
     for (int j = 0; j < s.world && !to; ++j) wait_tag(done_slot(s, s.rank, j), seq, 0, s, &to);
     if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
-}
-
-template <int W>
-__global__ void __launch_bounds__(512, 2) avg_kernel(SymmArgs s, uint64_t seq) {
-    average_shard<W>(s);
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
-        end_barrier(s, seq);
-        *s.arrive = 0u;
-        *s.seq = static_cast<uint32_t>(seq);
-    }
 }
 
 // agreed word of step `seq` from the N seq-tagged votes in this rank's signal slots
@@ -240,15 +220,19 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     }
 }
 
-// update-first order: K13 over the whole buffer, vote exchange in the last
-// block, the mean as a device-side launch on sync (separate function so the
-// streaming loop keeps its registers)
+// update-first order: K13 over the whole buffer; the last block to arrive
+// runs K2 and the vote exchange and broadcasts the agreed word to the other
+// blocks of the grid (all co-resident: one wave), which wait for it instead
+// of exiting. On sync every block then averages its part of this rank's
+// shard (C2, 1/N in the epilogue) and the last one runs the end barrier --
+// no second launch, no device-side launch.
 template <bool MOM, bool NEST, int W>
 __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
-                                     const Grids& gr, uint64_t seq) {
+                                     uint64_t seq) {
     __shared__ bool s_last;
+    __shared__ int s_w;
     uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;
-    // ---- update first: K13 over the whole buffer, vote in the last block
+    uint64_t* decided = reinterpret_cast<uint64_t*>(static_cast<char*>(f.ws) + 192);  // (seq << 32) | word
     const double acc = sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
     Workspace ws = ws_view(f.ws);
     const double bsum = block_sum(acc);
@@ -261,35 +245,48 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
         s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    double v = 0.0;
-    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
-    v = block_sum(v);
-    if (threadIdx.x != 0) return;
-    *ws.counter = 0u;
-    signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
-    const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+    if (s_last) {
+        __threadfence();
+        double v = 0.0;
+        for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
+        v = block_sum(v);
+        if (threadIdx.x == 0) {
+            *ws.counter = 0u;
+            signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+            const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+            __threadfence_system();
+            for (int j = 0; j < s.world; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
+            if (mark) mark[1] = now_ns();
+            const int w = agreed_vote(s, seq);
+            if (mark) mark[2] = now_ns();
+            *f.word = w;
+            if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
+            if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (w == SS_FLAG_SYNC ? 0.25f : 0.0f);
+            st_release_gpu(decided, (seq << 32) | static_cast<uint32_t>(w));
+            s_w = w;
+        }
+    } else if (threadIdx.x == 0) {
+        bool to = false;
+        const uint64_t t = wait_tag_gpu(decided, seq, s.timeout_ns, &to);
+        s_w = to ? -1 : static_cast<int>(static_cast<uint32_t>(t));
+    }
+    __syncthreads();
+    if (s_w != SS_FLAG_SYNC) {
+        if (s_last && threadIdx.x == 0) *s.seq = static_cast<uint32_t>(seq);
+        return;
+    }
+    average_shard<W>(s);
     __threadfence_system();
-    for (int j = 0; j < s.world; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
-    if (mark) mark[1] = now_ns();
-    const int w = agreed_vote(s, seq);
-    if (mark) mark[2] = now_ns();
-    *f.word = w;
-    if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
-    const bool sync = w == SS_FLAG_SYNC;
-    if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (sync ? 0.25f : 0.0f);
-    if (sync) {
-        if (o.child_launches) atomicAdd(o.child_launches, 1u);
-        avg_kernel<W><<<gr.avg, 512, 0, cudaStreamTailLaunch>>>(s, seq);
-    } else {
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+        end_barrier(s, seq);
+        *s.arrive = 0u;
         *s.seq = static_cast<uint32_t>(seq);
     }
 }
 
 template <bool MOM, bool NEST, int W>
-__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o,
-                                                            Grids gr) {
+__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     // the order of this step: identical on every rank (same decision history)
     const bool norm_first = o.mode == 1 || (o.mode == 2 && *reinterpret_cast<volatile float*>(o.predictor) >= o.threshold);
@@ -299,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
         nf_body<MOM, NEST, W>(a, f, s, o, seq);
         return;
     }
-    uf_body<MOM, NEST, W>(a, f, s, o, gr, seq);
+    uf_body<MOM, NEST, W>(a, f, s, o, seq);
 }
 
 // ------------------------------------------- gradient aggregation, one launch
@@ -418,26 +415,16 @@ int occupancy(K kernel, int threads) {
 
 template <bool MOM, bool NEST, int W>
 int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, void* stream) {
-    static int res_step = 0, res_avg = 0;
-    if (res_step == 0) {
-        res_step = occupancy(step_kernel<MOM, NEST, W>, kThreads);
-        res_avg = occupancy(avg_kernel<W>, 512);
-    }
-    const int sms = ss_internal::sm_count();
+    static int res_step = 0;
+    if (res_step == 0) res_step = occupancy(step_kernel<MOM, NEST, W>, kThreads);
+    // one wave (grid_for caps at #SMs x resident blocks): blocks wait on each
+    // other (decision broadcast, tickets), so every block must be co-resident
     const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res_step));
     f.total_blocks = grid;
-    Grids gr;
-    // averaging grid: every block co-resident (the last one runs the end barrier)
-    gr.avg = sms * res_avg;
-    const int64_t per_rank_vec = ((sa.n >> 2) + sa.world - 1) / sa.world;
-    const int64_t want = (per_rank_vec + 512 * 4 - 1) / (512 * 4);
-    if (want < gr.avg) gr.avg = static_cast<int>(want < 1 ? 1 : want);
-    gr.upd = 0;
-    gr.ua = 0;
     // norm-first pass: the in-flight window is ~grid tickets = grid / (N + 1)
     // groups; the mean of a tile is scheduled one window after its update
     o.lag = grid / (sa.world + 1) + 2;
-    step_kernel<MOM, NEST, W><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, f, sa, o, gr);
+    step_kernel<MOM, NEST, W><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, f, sa, o);
     return check_launch("ss_step_symm_f32");
 }
 
@@ -490,7 +477,6 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
     if (rc) return rc;
     if (grp->bufs[grp->rank] != w) return fail(SS_ERR_CONFIG, "w must be this rank's symmetric buffer");
     OverlapArgs o{};
-    o.child_launches = grp->child_launches;
     o.dbg = grp->debug_events;
     o.dbg_cap = grp->debug_events ? grp->debug_cap : 0;
     o.mode = grp->order_mode;

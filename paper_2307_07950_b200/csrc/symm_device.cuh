@@ -85,6 +85,35 @@ __device__ uint64_t wait_tag(const uint64_t* p, uint64_t want, int shift, const 
     return v;
 }
 
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// spin (bounded) until a gpu-scope tag (*p >> 32) == want; returns the last
+// value. Up to a few hundred blocks poll one word while the slowest blocks
+// still stream: relaxed polls with a back-off keep that traffic light, one
+// acquire fence after the match orders what follows.
+__device__ uint64_t wait_tag_gpu(const uint64_t* p, uint64_t want, uint64_t timeout_ns, bool* timed_out) {
+    const uint64_t t0 = now_ns();
+    uint64_t v = ld_relaxed_gpu(p);
+    while ((v >> 32) != want) {
+        if (now_ns() - t0 > timeout_ns) {
+            *timed_out = true;
+            return v;
+        }
+        __nanosleep(256);
+        v = ld_relaxed_gpu(p);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    return v;
+}
+
 // Signal slots of rank `owner`'s region. Votes are double-buffered by the
 // parity of the step tag: a fast rank may post its vote for step s+1 before a
 // slow rank has read the step-s votes, but never for s+2 (that needs the slow

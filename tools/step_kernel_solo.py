@@ -35,9 +35,13 @@ for _ in range(5):
 st.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 n = 20
+graph = st.capture(0.01) if os.environ.get("GRAPH") else None  # launch-bound sizes: one graph per step
 a.record()
 for _ in range(n):
-    st.step_async(0.01)
+    if graph is not None:
+        graph.replay()
+    else:
+        st.step_async(0.01)
 b.record()
 st.synchronize()
 ms = a.elapsed_time(b) / n
