@@ -7,9 +7,17 @@ parameters, SGD with momentum 0.9 and weight decay 4e-4 (the paper's
 ResNet-101 optimizer), synthetic gradients already resident
 in HBM. A step is the whole hot path:
 
-  K13+K2 (fused update + ||g||^2 + EWMA/Delta/decide, one kernel)
-  -> C1 NCCL allreduce-MAX of the flag word
-  -> C2 NCCL allreduce-AVG of the 400 MB parameter buffer on sync steps.
+  K13+K2 (fused update + ||g||^2 + EWMA/Delta/decide)
+  -> C1 flag-word MAX over ranks
+  -> C2 mean of the 400 MB parameter buffer on sync steps.
+
+At N = 1 that is one K13 launch. At N > 1 (default --collective symm
+--flag-exchange fused) it is ONE launch of the symmetric-memory step kernel
+(ss_step_symm_f32): C1 as a seq-tagged NVLink P2P vote and C2 as an NVLS
+multicast (N >= 4) or P2P two-shot (N = 2) mean with 1/N in registers,
+overlapped tile by tile with the update in the norm-first order.
+``--collective nccl`` is the literal north_star variant (NCCL allreduce-MAX
+of an int32 word, NCCL allreduce-AVG of the buffer) kept for comparison.
 
 The headline ``value`` is steps/s of the whole job under a decision mix with
 exactly 50% sync steps (gradient ring with scales [1, 1, 1.5, 1.5], EWMA
