@@ -1,5 +1,7 @@
 """Where does a local step's time go at N > 1 (update-first order)? Device
-timestamps of: step kernel start, vote posted (last block), all votes in."""
+timestamps of: step kernel start, vote posted (last block), all votes in.
+Args: P, steps enqueued back to back per sample (marks are of the last one;
+the event time is per step)."""
 import os
 import sys
 from pathlib import Path
@@ -12,7 +14,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2307_07950_b200 import SelSyncConfig  # noqa: E402
 from paper_2307_07950_b200.step import SelSyncStep  # noqa: E402
 
-P = 100_000_000
+P = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+B2B = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # steps enqueued back to back per sample
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 local = int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -29,11 +32,12 @@ rows = []
 for _ in range(20):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    st.step_async(0.001)
+    for _ in range(B2B):
+        st.step_async(0.001)
     b.record()
     st.synchronize()
     mk = tl.cpu().numpy()[4 * 16:]
-    rows.append(((mk[1] - mk[0]) / 1e3, (mk[2] - mk[1]) / 1e3, a.elapsed_time(b) * 1e3, mk[0], mk[1]))
+    rows.append(((mk[1] - mk[0]) / 1e3, (mk[2] - mk[1]) / 1e3, a.elapsed_time(b) * 1e3 / B2B, mk[0], mk[1]))
 r = np.array(rows)
 txt = (f"rank {rank}: start->vote posted {r[:,0].mean():.1f} us, vote wait {r[:,1].mean():.1f} us "
        f"(max {r[:,1].max():.1f}), event step {r[:,2].mean():.1f} us")
