@@ -211,13 +211,15 @@ typedef struct ss_symm_group {
          1  norm first: K1, vote, then on sync ONE kernel that overlaps the update
             of each tile with the NVLink mean of tiles all ranks have finished
             (on local steps the plain update);
-         2  adaptive: order 1 while an EWMA of the agreed decisions >= threshold.
+         2  adaptive: order 1 when the predicted sync probability >= threshold (EWMA of
+            the agreed decisions per context of the previous two).
        Both orders compute identical parameters. Order 1/2 needs the fields below. */
     int32_t order_mode;
     float order_threshold;
     uint32_t* tile_cnt[SS_SYMM_MAX_RANKS]; /* rank r's per-tile arrival counters (peer-mapped, zeroed) */
     uint32_t* epoch;                    /* overlapped sync steps completed (zeroed) */
-    float* predictor;                   /* EWMA of agreed sync decisions (zeroed) */
+    float* predictor;                   /* 5 floats, zeroed: P(sync) EWMA per context of the
+                                           last two agreed decisions, then the context */
     int64_t tile_elems;                 /* elements per tile, multiple of 4 */
     int64_t n_tiles;                    /* capacity of every tile_cnt array */
     void* reserved0;                    /* unused (layout slot), pass NULL */

@@ -178,7 +178,8 @@ class SymmetricParams:
         for r, p in enumerate(self.cnt_hdl.buffer_ptrs):
             g.tile_cnt[r] = int(p)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.predictor = torch.zeros(1, dtype=torch.float32, device=self.device)
+        # order predictor: P(sync) per context of the last two agreed decisions + the context
+        self.predictor = torch.zeros(5, dtype=torch.float32, device=self.device)
         g.epoch = self.epoch.data_ptr()
         g.predictor = self.predictor.data_ptr()
         g.tile_elems = int(tile_elems)

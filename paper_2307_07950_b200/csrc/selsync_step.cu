@@ -48,7 +48,7 @@ namespace {
 struct OverlapArgs {
     uint32_t* cnt[kMaxRanks];  // per-rank tile arrival counters, indexed by tile
     uint32_t* epoch;
-    float* predictor;
+    float* predictor;          // kPredictorFloats: P(sync) per 2-decision context + the context
     int mode;
     float threshold;
     int64_t tile;
@@ -67,6 +67,24 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Order predictor (adaptive mode): P(sync) per context of the last two agreed
+// decisions, each an EWMA (weight 1/4) of the decisions that followed that
+// context; pr[4] holds the context (0..3). A 2-bit history learns runs
+// (context LL -> local, SS -> sync) as well as alternations, where a single
+// EWMA would sit near 0.5 and pick the norm-first order for every local step.
+// Every rank updates it from the same agreed words: all ranks pick the same order.
+constexpr int kPredictorFloats = 5;
+__device__ __forceinline__ float predicted_sync(const float* pr) {
+    const int h = static_cast<int>(reinterpret_cast<const volatile float*>(pr)[4]) & 3;
+    return reinterpret_cast<const volatile float*>(pr)[h];
+}
+__device__ __forceinline__ void predictor_update(float* pr, int w) {
+    const int h = static_cast<int>(pr[4]) & 3;
+    const int s = w == SS_FLAG_SYNC ? 1 : 0;
+    pr[h] = 0.75f * pr[h] + (s ? 0.25f : 0.0f);
+    pr[4] = static_cast<float>(((h << 1) | s) & 3);
 }
 
 // end of a sync step on this rank: done tags to every peer, wait for all
@@ -210,7 +228,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
         if (o.dbg) o.dbg[4 * o.dbg_cap + 4] = now_ns();
         *f.word = w;
         if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
-        if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (w == SS_FLAG_SYNC ? 0.25f : 0.0f);
+        if (o.mode == 2) predictor_update(o.predictor, w);
         if (w == SS_FLAG_SYNC) end_barrier(s, seq);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 5] = now_ns();
         *o.ticket = 0ull;
@@ -261,7 +279,7 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
             if (mark) mark[2] = now_ns();
             *f.word = w;
             if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
-            if (o.mode == 2) *o.predictor = 0.75f * *o.predictor + (w == SS_FLAG_SYNC ? 0.25f : 0.0f);
+            if (o.mode == 2) predictor_update(o.predictor, w);
             st_release_gpu(decided, (seq << 32) | static_cast<uint32_t>(w));
             s_w = w;
         }
@@ -289,7 +307,7 @@ template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     // the order of this step: identical on every rank (same decision history)
-    const bool norm_first = o.mode == 1 || (o.mode == 2 && *reinterpret_cast<volatile float*>(o.predictor) >= o.threshold);
+    const bool norm_first = o.mode == 1 || (o.mode == 2 && predicted_sync(o.predictor) >= o.threshold);
     uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {start, vote posted, votes in, -, last arrival, end}
     if (mark && blockIdx.x == 0 && threadIdx.x == 0) mark[0] = now_ns();
     if (norm_first) {

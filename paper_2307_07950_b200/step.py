@@ -38,6 +38,7 @@ K1+K2, C1, then on sync allreduce-AVG of the gradients, then the update.
 from __future__ import annotations
 
 import math
+from collections import deque
 from typing import Optional
 
 import torch
@@ -133,8 +134,11 @@ class SelSyncStep:
         self._word_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._ready = torch.cuda.Event()
         self.steps_done = 0
+        # host-side per-step log, bounded to the trace-ring window (records() /
+        # decisions() cover the last trace_capacity steps): decisions the host
+        # learned in blocking steps, and the lr of every step
         self._host_decisions: dict[int, bool] = {}
-        self.lrs: list[float] = []
+        self._lr_ring: list[float] = [0.0] * self.signal.trace_capacity
         self.profile = profile
         self.kernel_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
         self.sync_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
@@ -245,8 +249,16 @@ class SelSyncStep:
             raise ConfigError("step_async needs collective='symm' (or a single rank)")
         lr = self._check_lr(lr)
         self._enqueue_device_step(lr, torch.cuda.current_stream(self.device))
-        self.steps_done += 1
-        self.lrs.append(lr)
+        self._log_step(lr)
+
+    def _log_step(self, lr: float, synced: Optional[bool] = None) -> None:
+        """Advance the step counter, keeping the host log within the ring window."""
+        s, cap = self.steps_done, self.signal.trace_capacity
+        if synced is not None:
+            self._host_decisions[s] = synced
+        self._host_decisions.pop(s - cap, None)
+        self._lr_ring[s % cap] = lr
+        self.steps_done = s + 1
 
     def step(self, lr: float) -> str:
         """Run one SelSync step on the gradients in ``grads``; returns the
@@ -302,9 +314,7 @@ class SelSyncStep:
                     self.comm.average_(self.grads)
                 K.sgd_update_(self.params, self.grads, self.momentum, lr=lr, **self._hp(first))
         synced = bool(word & 1)
-        self._host_decisions[self.steps_done] = synced
-        self.steps_done += 1
-        self.lrs.append(lr)
+        self._log_step(lr, synced)
         return "sync" if synced else "local"
 
     def capture(self, lr: float) -> "CapturedStep":
@@ -390,7 +400,7 @@ class SelSyncStep:
                 step=step, worker_id=self.worker_id, grad_norm_sq=float(r["grad_norm_sq"]),
                 ewma=float(r["ewma"]), delta_g=None if math.isnan(d) else d,
                 decision="sync" if dec[i] else "local",
-                vote=bool(int(r["word"]) & 1), lr=self.lrs[step]))
+                vote=bool(int(r["word"]) & 1), lr=self._lr_ring[step % cap]))
         return out
 
     def kernel_ms(self) -> list[float]:
@@ -408,8 +418,7 @@ class CapturedStep:
 
     def replay(self) -> None:
         self.graph.replay()
-        self.step.steps_done += 1
-        self.step.lrs.append(self.lr)
+        self.step._log_step(self.lr)
         K._count()
 
 
@@ -446,7 +455,7 @@ class TensorListSelSyncStep:
         self._word_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self._ready = torch.cuda.Event()
         self.steps_done = 0
-        self.decision_log: list[bool] = []
+        self.decision_log: deque = deque(maxlen=trace_capacity)  # last trace_capacity decisions
         if broadcast_init and self.world > 1:
             for p in self.params:
                 self.comm.broadcast_(p, 0)

@@ -91,7 +91,6 @@ class SelSyncTrainer:
             torch.cuda.synchronize(self.step.device)
             self._record_graph()
         self.graph.replay()
-        self.step.steps_done += 1
-        self.step.lrs.append(lr)
+        self.step._log_step(lr)
         self.iteration += 1
         return self.static_loss

@@ -41,7 +41,7 @@ for order, alt, bc, pin in variants:
             pred = -1.0
         else:
             g.copy_(torch.from_numpy(O.synthetic_grad32(c["grad_seed"], rank, s, P)))
-            pred = float(st.symm.predictor.item())
+            pred = float(st.symm.predictor[int(st.symm.predictor[4].item()) & 3].item())
         try:
             if alt and s % 2:
                 st.step_async(c["lr"])
