@@ -77,8 +77,11 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
 // Every rank updates it from the same agreed words: all ranks pick the same order.
 constexpr int kPredictorFloats = 5;
 __device__ __forceinline__ float predicted_sync(const float* pr) {
-    const int h = static_cast<int>(reinterpret_cast<const volatile float*>(pr)[4]) & 3;
-    return reinterpret_cast<const volatile float*>(pr)[h];
+    // five independent loads, then a select: no dependent load at kernel start
+    const volatile float* v = pr;
+    const float p0 = v[0], p1 = v[1], p2 = v[2], p3 = v[3];
+    const int h = static_cast<int>(v[4]) & 3;
+    return h == 0 ? p0 : h == 1 ? p1 : h == 2 ? p2 : p3;
 }
 __device__ __forceinline__ void predictor_update(float* pr, int w) {
     const int h = static_cast<int>(pr[4]) & 3;
