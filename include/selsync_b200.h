@@ -222,7 +222,8 @@ typedef struct ss_symm_group {
                                            last two agreed decisions, then the context */
     int64_t tile_elems;                 /* elements per tile, multiple of 4 */
     int64_t n_tiles;                    /* capacity of every tile_cnt array */
-    void* reserved0;                    /* unused (layout slot), pass NULL */
+    double* tile_norm;                  /* optional, n_tiles doubles: per-tile ||g||^2 partials of the
+                                           known-sync pass (warmup steps, delta == 0); NULL disables it */
     uint64_t* debug_events;             /* optional: per-ticket timeline of the overlapped step */
     int64_t debug_cap;                  /* tickets recorded (4 x uint64 each) */
 } ss_symm_group;

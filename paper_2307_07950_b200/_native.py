@@ -8,6 +8,7 @@ CUDA tensor. Build it with ``python -m paper_2307_07950_b200._build``.
 from __future__ import annotations
 
 import ctypes
+import os
 from ctypes import (
     POINTER,
     Structure,
@@ -23,7 +24,8 @@ from pathlib import Path
 
 from .errors import ConfigError, SignalError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libselsync_b200.so"
+# SS_LIB_PATH: load another build of the library (A/B timing of two builds on one box)
+LIB_PATH = Path(os.environ.get("SS_LIB_PATH") or Path(__file__).resolve().parent / "_lib" / "libselsync_b200.so")
 
 SS_OK, SS_ERR_CONFIG, SS_ERR_SIGNAL, SS_ERR_CUDA = 0, 1, 2, 3
 SS_FLAG_SYNC, SS_FLAG_ERR_NAN, SS_FLAG_ERR_NEG = 1, 2, 4
@@ -86,7 +88,7 @@ class SymmGroupC(Structure):
         ("predictor", c_void_p),
         ("tile_elems", c_int64),
         ("n_tiles", c_int64),
-        ("reserved0", c_void_p),
+        ("tile_norm", c_void_p),
         ("debug_events", c_void_p),
         ("debug_cap", c_int64),
     ]

@@ -16,6 +16,7 @@ CPU tensors, which the world-size-2 CPU tests use.
 
 from __future__ import annotations
 
+import os
 from typing import Optional
 
 import torch
@@ -177,6 +178,12 @@ class SymmetricParams:
         self.cnt.zero_()
         for r, p in enumerate(self.cnt_hdl.buffer_ptrs):
             g.tile_cnt[r] = int(p)
+        # known-sync pass (warmup steps, delta == 0): ||g||^2 partial per update
+        # tile; SS_KNOWN_SYNC=0 disables the pass (A/B knob)
+        self.tile_norm = None
+        if os.environ.get("SS_KNOWN_SYNC", "1") != "0":
+            self.tile_norm = torch.zeros(max(1, self.n_tiles), dtype=torch.float64, device=self.device)
+            g.tile_norm = self.tile_norm.data_ptr()
         self.epoch = torch.zeros(1, dtype=torch.int32, device=self.device)
         # order predictor: P(sync) per context of the last two agreed decisions + the context
         self.predictor = torch.zeros(5, dtype=torch.float32, device=self.device)

@@ -374,13 +374,15 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
 // The update over elements [e0, e1) by the threads of ONE block (tile work of
 // the overlapped sync step). Requires 16-byte-aligned streams (head == 0) and
 // e0 % 4 == 0; a scalar tail is handled when e1 is not a multiple of 4.
-template <bool MOM, bool NEST, int U = 2, bool G_L2 = false>
-__device__ __forceinline__ void sgd_block_range(const SgdArgs& a, int64_t e0, int64_t e1) {
+// NORM: also return this thread's fp64 partial of ||g||^2 over the range.
+template <bool MOM, bool NEST, int U = 2, bool G_L2 = false, bool NORM = false>
+__device__ __forceinline__ double sgd_block_range(const SgdArgs& a, int64_t e0, int64_t e1) {
     // G_L2: read g through L2 only (it was just rewritten by peers over NVLink)
     // U vectors per stream in flight per thread: in the overlapped step only
     // part of the grid updates at a time, so each block needs more bytes in
     // flight than in the whole-grid K13 sweep (where U = 1 is best)
     const float s = 1.0f;
+    double acc = 0.0;
     const int64_t v0 = e0 >> 2, v1 = e1 >> 2;
     const int64_t bs = blockDim.x;
     int64_t i = v0 + threadIdx.x;
@@ -396,6 +398,7 @@ __device__ __forceinline__ void sgd_block_range(const SgdArgs& a, int64_t e0, in
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t k = 4 * (i + u * bs);
+            if (NORM) acc = sq4(gv[u], acc);
             float4 mm = MOM ? mv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
             sgd_elem<MOM, NEST>(wv[u].x, gv[u].x, mm.x, a, s);
             sgd_elem<MOM, NEST>(wv[u].y, gv[u].y, mm.y, a, s);
@@ -410,6 +413,7 @@ __device__ __forceinline__ void sgd_block_range(const SgdArgs& a, int64_t e0, in
         float4 gv = G_L2 ? __ldcg(reinterpret_cast<const float4*>(a.g + k)) : ld_cs4(a.g + k);
         float4 wv = ld_cs4(a.w + k);
         float4 mm = MOM ? ld_cs4(a.m + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (NORM) acc = sq4(gv, acc);
         sgd_elem<MOM, NEST>(wv.x, gv.x, mm.x, a, s);
         sgd_elem<MOM, NEST>(wv.y, gv.y, mm.y, a, s);
         sgd_elem<MOM, NEST>(wv.z, gv.z, mm.z, a, s);
@@ -421,10 +425,12 @@ __device__ __forceinline__ void sgd_block_range(const SgdArgs& a, int64_t e0, in
     for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += bs) {
         float w = a.w[j], g = G_L2 ? __ldcg(a.g + j) : a.g[j];
         float m = MOM ? a.m[j] : 0.0f;
+        if (NORM) acc = fma(static_cast<double>(g), static_cast<double>(g), acc);
         sgd_elem<MOM, NEST>(w, g, MOM ? m : mdummy, a, s);
         a.w[j] = w;
         if (MOM) a.m[j] = m;
     }
+    return acc;
 }
 
 }  // namespace

@@ -25,9 +25,19 @@
 //     HBM-bound update overlaps the NVLink-bound mean tile by tile. Tickets
 //     only wait on earlier tickets, so the pass cannot deadlock.
 //
-//  adaptive (order 2): the last block keeps an EWMA of the agreed decisions;
-//     the next step uses order 1 while it is >= threshold. Both orders
-//     compute identical parameters (same per-element arithmetic).
+//  adaptive (order 2): the last block keeps, per context of the previous two
+//     agreed decisions, an EWMA of the decision that followed; the next step
+//     uses order 1 when the prediction for the current context is >= threshold.
+//
+//  known sync (orders 1 and 2, with tile_norm): when the step is sync whatever
+//     ||g||^2 turns out to be (warmup, or delta == 0), the ticketed pass runs
+//     without the norm sweep and without waiting for the vote: each update
+//     tile also yields its ||g||^2 partial, the block finishing the last tile
+//     reduces them in tile order, runs K2 and posts the vote (still exchanged,
+//     for the trace, the EWMA and NaN error bits); the mean overlaps the
+//     update from the first tiles on. 20P HBM bytes instead of 24P.
+//
+//  All orders compute identical parameters (same per-element arithmetic).
 
 #include "selsync_b200.h"
 #include "common.cuh"
@@ -48,7 +58,7 @@ namespace {
 struct OverlapArgs {
     uint32_t* cnt[kMaxRanks];  // per-rank tile arrival counters, indexed by tile
     uint32_t* epoch;
-    float* predictor;          // kPredictorFloats: P(sync) per 2-decision context + the context
+    float* predictor;          // 5 floats: P(sync) per 2-decision context + the context
     int mode;
     float threshold;
     int64_t tile;
@@ -57,6 +67,7 @@ struct OverlapArgs {
     unsigned long long* ticket;
     uint64_t* dbg;             // optional per-ticket timeline: {kind << 48 | tile, t0, t_ready, t_end}
     int64_t dbg_cap;
+    double* tile_norm;         // known-sync pass: ||g||^2 partial per tile (NULL: pass disabled)
 };
 
 __device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
@@ -75,7 +86,6 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
 // (context LL -> local, SS -> sync) as well as alternations, where a single
 // EWMA would sit near 0.5 and pick the norm-first order for every local step.
 // Every rank updates it from the same agreed words: all ranks pick the same order.
-constexpr int kPredictorFloats = 5;
 __device__ __forceinline__ float predicted_sync(const float* pr) {
     // five independent loads, then a select: no dependent load at kernel start
     const volatile float* v = pr;
@@ -114,9 +124,46 @@ __device__ int agreed_vote(const SymmArgs& s, uint64_t seq) {
     return w;
 }
 
+// Known-sync pass: called by every thread of the block that just finished an
+// update tile (its ||g||^2 partial is in tile_norm). The block finishing the
+// last tile of this rank reduces the partials in tile order (deterministic),
+// runs K2 and posts this rank's vote.
+__device__ void known_tile_done(const Finish& f, const SymmArgs& s, const OverlapArgs& o, uint64_t seq, int N,
+                                int64_t T) {
+    __shared__ bool s_last_tile;
+    Workspace ws = ws_view(f.ws);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last_tile = atomicAdd(ws.counter, 1u) == static_cast<unsigned int>(T - 1);
+    }
+    __syncthreads();
+    if (!s_last_tile) return;
+    __threadfence();
+    double v = 0.0;
+    for (int64_t i = threadIdx.x; i < T; i += blockDim.x) v += __ldcg(o.tile_norm + i);
+    v = block_sum(v);
+    if (threadIdx.x == 0) {
+        *ws.counter = 0u;
+        signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+        const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+        __threadfence_system();
+        for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
+        if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
+    }
+}
+
+// The decision of this step is sync before ||g||^2 is known: warmup (the
+// observation about to be made is number <= warmup, signal.py:105-106) or
+// delta == 0 (Delta >= 0 always). Same on every rank (same step count, delta).
+__device__ __forceinline__ bool sync_known_ahead(const Finish& f) {
+    if (f.delta == 0.0) return true;
+    const volatile ss_signal_state* st = f.st;
+    return st->step_count + 1 <= static_cast<int64_t>(st->warmup);
+}
+
 template <bool MOM, bool NEST, int W>
 __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
-                                     uint64_t seq) {
+                                     uint64_t seq, bool known) {
     __shared__ unsigned long long s_ticket;
     __shared__ int s_vote;
     __shared__ bool s_last;
@@ -126,11 +173,16 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     const unsigned long long total = static_cast<unsigned long long>(groups) * (N + 1);
     const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(o.epoch) + 1;
     const uint32_t target = static_cast<uint32_t>(N) * epoch;
-    if (threadIdx.x == 0) s_vote = -2;
+    // known: the decision is sync whatever ||g||^2 turns out to be (warmup or
+    // delta == 0, identical on every rank), so the mean tickets need no vote;
+    // ||g||^2 then comes from the update tiles themselves (no separate sweep)
+    // and the vote is still exchanged at the end, for the trace, the EWMA and
+    // the error bits.
+    if (threadIdx.x == 0) s_vote = known ? SS_FLAG_SYNC : -2;
     // ---- phase 1: ||g||^2 by the whole grid (full-speed sweep); the last block
     //      to arrive reduces the partials in a fixed order, runs K2 and posts the
     //      vote. Nobody waits here: blocks go straight on to the update tickets.
-    {
+    if (!known) {
         Workspace ws = ws_view(f.ws);
         const double bsum = block_sum(norm_pass<4>(a.g, a.n, a.head));
         if (threadIdx.x == 0) {
@@ -181,11 +233,18 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                 const int64_t t = grp * N + pos;
                 if (t < T) {
                     const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
-                    sgd_block_range<MOM, NEST>(a, e0, e1);
-                    __syncthreads();
+                    if (!known) {
+                        sgd_block_range<MOM, NEST>(a, e0, e1);
+                        __syncthreads();
+                    } else {
+                        // block_sum's barriers also order the block's stores
+                        const double ts = block_sum(sgd_block_range<MOM, NEST, 1, false, true>(a, e0, e1));
+                        if (threadIdx.x == 0) o.tile_norm[t] = ts;
+                    }
                     // release at sys scope: the block's stores (ordered by the
                     // barrier) are visible to the owner before the count
                     if (threadIdx.x == 0) red_add_release_sys(o.cnt[t % N] + t, 1u);
+                    if (known) known_tile_done(f, s, o, seq, N, T);
                     rec_tile = t;
                 }
             } else {
@@ -227,12 +286,12 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
-        const int w = s_vote != -2 ? s_vote : agreed_vote(s, seq);
+        const int w = (s_vote != -2 && !known) ? s_vote : agreed_vote(s, seq);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 4] = now_ns();
         *f.word = w;
         if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
         if (o.mode == 2) predictor_update(o.predictor, w);
-        if (w == SS_FLAG_SYNC) end_barrier(s, seq);
+        if (w == SS_FLAG_SYNC || known) end_barrier(s, seq);  // known: the mean ran in any case
         if (o.dbg) o.dbg[4 * o.dbg_cap + 5] = now_ns();
         *o.ticket = 0ull;
         *o.epoch = epoch;
@@ -310,11 +369,12 @@ template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     // the order of this step: identical on every rank (same decision history)
-    const bool norm_first = o.mode == 1 || (o.mode == 2 && predicted_sync(o.predictor) >= o.threshold);
+    const bool known = o.mode != 0 && o.tile_norm != nullptr && sync_known_ahead(f);
+    const bool norm_first = known || o.mode == 1 || (o.mode == 2 && predicted_sync(o.predictor) >= o.threshold);
     uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {start, vote posted, votes in, -, last arrival, end}
     if (mark && blockIdx.x == 0 && threadIdx.x == 0) mark[0] = now_ns();
     if (norm_first) {
-        nf_body<MOM, NEST, W>(a, f, s, o, seq);
+        nf_body<MOM, NEST, W>(a, f, s, o, seq, known);
         return;
     }
     uf_body<MOM, NEST, W>(a, f, s, o, seq);
@@ -518,6 +578,7 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
         o.tile = grp->tile_elems;
         o.n_tiles = tiles;
         o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
+        o.tile_norm = grp->tile_norm;
     }
     Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
     const bool mom = momentum != 0.0f, nest = nesterov != 0;

@@ -83,6 +83,11 @@ def large_aggregation(variant):
     return "grads" if variant.startswith("ga") else "params"
 
 
+def large_delta(variant):
+    """bsp: delta = 0, every step sync -- known before ||g||^2 (the known-sync pass)."""
+    return 0.0 if variant == "bsp" else LARGE["delta"]
+
+
 def large_main():
     """Many tiles and a ragged tail: P = 1,000,003 with 4096-element tiles
     (245 tiles, lag groups, a 3-element scalar tail), momentum + weight decay,
@@ -96,7 +101,8 @@ def large_main():
             "nvls-mean": dict(collective="symm", flag_exchange="fused", order="adaptive", multicast=True),
             "two-launch": dict(collective="symm", flag_exchange="p2p"),
             "ga": dict(collective="symm", flag_exchange="fused"),
-            "ga-nccl": dict(collective="nccl", fuse=True)}[variant]
+            "ga-nccl": dict(collective="nccl", fuse=True),
+            "bsp": dict(collective="symm", flag_exchange="fused", order="adaptive")}[variant]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -106,8 +112,9 @@ def large_main():
     P = c["P"]
     init = torch.from_numpy(large_init(c["seed"], P)).to(dev)
     g = torch.zeros(P, device=dev)
-    cfg = SelSyncConfig(delta=c["delta"], warmup=c["warmup"], smoothing=c["smoothing"], momentum=c["momentum"],
-                        weight_decay=c["weight_decay"], aggregation=large_aggregation(variant))
+    cfg = SelSyncConfig(delta=large_delta(variant), warmup=c["warmup"], smoothing=c["smoothing"],
+                        momentum=c["momentum"], weight_decay=c["weight_decay"],
+                        aggregation=large_aggregation(variant))
     step = SelSyncStep(init, g, cfg, tile_elems=c["tile"], **opts)
     g = step.grads  # gradient aggregation over symmetric memory owns the gradient buffer
     for s in range(c["steps"]):

@@ -67,21 +67,21 @@ def large_oracle():
     c = MW.LARGE
     cache = {}
 
-    def get(n, aggregation):
-        if (n, aggregation) not in cache:
+    def get(n, aggregation, delta):
+        if (n, aggregation, delta) not in cache:
             init = MW.large_init(c["seed"], c["P"]).astype(np.float64)
-            cache[n, aggregation] = O.simulate_selsync(
+            cache[n, aggregation, delta] = O.simulate_selsync(
                 init, n, c["steps"], lambda w, s, _p: O.synthetic_grad32(c["seed"], w, s, c["P"]).astype(np.float64),
-                delta=c["delta"], warmup=c["warmup"], smoothing=c["smoothing"], lr=c["lr"], momentum=c["momentum"],
+                delta=delta, warmup=c["warmup"], smoothing=c["smoothing"], lr=c["lr"], momentum=c["momentum"],
                 weight_decay=c["weight_decay"], aggregation=aggregation)
-        return cache[n, aggregation]
+        return cache[n, aggregation, delta]
     return get
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("n", [2, 4])
 @pytest.mark.parametrize("variant", ["nccl", "update_first", "norm_first", "adaptive", "p2p-mean", "nvls-mean",
-                                     "two-launch", "ga", "ga-nccl"])
+                                     "two-launch", "ga", "ga-nccl", "bsp"])
 def test_large_ragged_many_tiles_match_oracle(n, variant, tmp_path, large_oracle):
     """P = 1,000,003 in 4096-element tiles, momentum + weight decay, mixed
     decisions: the tile tickets, lag groups, scalar tail and every back end
@@ -95,11 +95,15 @@ def test_large_ragged_many_tiles_match_oracle(n, variant, tmp_path, large_oracle
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     import mp_selsync_worker as MW
 
-    ref = large_oracle(n, MW.large_aggregation(variant))
+    delta = MW.large_delta(variant)
+    ref = large_oracle(n, MW.large_aggregation(variant), delta)
     for rank in range(n):
         z = np.load(tmp_path / f"large_{variant}_rank{rank}.npz")
-        assert_trace_parity(z["decisions"], ref.decision, ref.delta_g, MW.LARGE["delta"], MW.LARGE["warmup"])
+        assert_trace_parity(z["decisions"], ref.decision, ref.delta_g, delta, MW.LARGE["warmup"])
         np.testing.assert_allclose(z["ewma"], ref.ewma[:, rank], rtol=1e-5)
         params_close(z["params"], ref.finals[rank])
-    assert 0 < int(np.sum(z["decisions"][MW.LARGE["warmup"]:])) < MW.LARGE["steps"] - MW.LARGE["warmup"], \
-        "case must mix sync and local steps"
+    if variant == "bsp":  # every step takes the known-sync pass (no norm sweep, no vote wait)
+        assert bool(np.all(z["decisions"])), "delta = 0 must sync every step"
+    else:
+        assert 0 < int(np.sum(z["decisions"][MW.LARGE["warmup"]:])) < MW.LARGE["steps"] - MW.LARGE["warmup"], \
+            "case must mix sync and local steps"
