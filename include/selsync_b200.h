@@ -93,6 +93,11 @@ SS_API int ss_signal_observe(ss_signal_state* st_host, double grad_norm_sq);
 SS_API int ss_relative_change(const ss_signal_state* st_host, double* out_host);
 /* decide, signal.py:101-107: *sync_out = 1 for "sync", 0 for "local" */
 SS_API int ss_decide(const ss_signal_state* st_host, double delta, int32_t* sync_out_host);
+/* *known_out = 1 when the NEXT decide (after one more observe of any finite
+   ||g||^2 >= 0) is "sync" whatever that norm is: a warmup step or delta == 0.
+   The one-launch step uses the same predicate on the device (known-sync pass).
+   No reference counterpart: it restates signal.py:101-107 one step ahead. */
+SS_API int ss_sync_known_ahead(const ss_signal_state* st_host, double delta, int32_t* known_out_host);
 
 /* ---------------- device hot path (sm_100a) ---------------- */
 

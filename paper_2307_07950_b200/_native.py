@@ -106,6 +106,7 @@ _SIGS = {
     "ss_signal_observe": ([POINTER(SignalStateC), c_double], c_int),
     "ss_relative_change": ([POINTER(SignalStateC), POINTER(c_double)], c_int),
     "ss_decide": ([POINTER(SignalStateC), c_double, POINTER(c_int32)], c_int),
+    "ss_sync_known_ahead": ([POINTER(SignalStateC), c_double, POINTER(c_int32)], c_int),
     "ss_workspace_bytes": ([POINTER(c_int64)], c_int),
     "ss_workspace_reset": ([_P, _P], c_int),
     "ss_norm_sq_f32": ([_P, c_int64, _P, _P, _P], c_int),

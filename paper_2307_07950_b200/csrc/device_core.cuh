@@ -123,6 +123,15 @@ __host__ __device__ inline int vote_core(const ss_signal_state* s, double delta)
     return rel_change_core(s->ewma_previous, s->ewma_current) >= delta ? 1 : 0;
 }
 
+// The decision after the NEXT observation is sync whatever the observed norm
+// (finite, >= 0): the observation about to be made is number <= warmup, or
+// delta == 0 (Delta >= 0 whenever it is defined, inf included). Sound and
+// complete: past warmup with delta > 0, observing x == ewma_current gives
+// Delta == 0 < delta (local). tests/test_signal_api.py checks both directions.
+__host__ __device__ inline bool sync_known_ahead_core(int64_t step_count, int32_t warmup, double delta) {
+    return delta == 0.0 || step_count + 1 <= static_cast<int64_t>(warmup);
+}
+
 // K2 body: one thread. Writes the flag word and the trace row.
 __device__ void signal_step_dev(ss_signal_state* st, double x, double delta, int32_t* word,
                                 ss_trace_row* trace, int32_t cap) {

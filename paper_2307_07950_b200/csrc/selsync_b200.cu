@@ -279,6 +279,14 @@ int ss_decide(const ss_signal_state* st, double delta, int32_t* sync_out) {
     return SS_OK;
 }
 
+int ss_sync_known_ahead(const ss_signal_state* st, double delta, int32_t* known_out) {
+    if (!st || !known_out) return fail(SS_ERR_CONFIG, "null argument");
+    int rc = check_delta_impl(delta);
+    if (rc) return rc;
+    *known_out = sync_known_ahead_core(st->step_count, st->warmup, delta) ? 1 : 0;
+    return SS_OK;
+}
+
 int ss_workspace_bytes(int64_t* bytes) {
     if (!bytes) return fail(SS_ERR_CONFIG, "null output");
     *bytes = kWsBytes;

@@ -158,7 +158,7 @@ __device__ void known_tile_done(const Finish& f, const SymmArgs& s, const Overla
 __device__ __forceinline__ bool sync_known_ahead(const Finish& f) {
     if (f.delta == 0.0) return true;
     const volatile ss_signal_state* st = f.st;
-    return st->step_count + 1 <= static_cast<int64_t>(st->warmup);
+    return sync_known_ahead_core(st->step_count, st->warmup, f.delta);
 }
 
 template <bool MOM, bool NEST, int W>

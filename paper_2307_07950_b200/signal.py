@@ -108,6 +108,17 @@ def decide(state: GradSignalState, threshold: DeltaThreshold) -> str:
     return "sync" if out.value else "local"
 
 
+def sync_known_ahead(state: GradSignalState, threshold: DeltaThreshold) -> bool:
+    """True when the decision after the next observation is "sync" whatever
+    the observed norm: a warmup step, or delta == 0. Not in the reference; the
+    one-launch step uses the same predicate to start the mean before ||g||^2
+    is known (DESIGN.md, known-sync pass)."""
+    c = state.to_c()
+    out = ctypes.c_int32(0)
+    N.check(N.LIB.ss_sync_known_ahead(ctypes.byref(c), float(threshold.delta), ctypes.byref(out)))
+    return bool(out.value)
+
+
 def replay_decisions(deltas, warmup: int, delta: float) -> int:
     """Count sync decisions of a recorded Delta trace at one threshold
     (signal.py:110-124); entries recorded during warmup are None."""
@@ -124,4 +135,5 @@ __all__ = [
     "observe",
     "relative_change",
     "replay_decisions",
+    "sync_known_ahead",
 ]
