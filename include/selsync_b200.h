@@ -218,7 +218,9 @@ typedef struct ss_symm_group {
             (on local steps the plain update);
          2  adaptive: order 1 when the predicted sync probability >= threshold (EWMA of
             the agreed decisions per context of the previous two).
-       Both orders compute identical parameters. Order 1/2 needs the fields below. */
+       Orders 1/2 with tile_norm also run the known-sync pass on steps whose
+       decision is sync before ||g||^2 is known (ss_sync_known_ahead).
+       All orders compute identical parameters. Order 1/2 needs the fields below. */
     int32_t order_mode;
     float order_threshold;
     uint32_t* tile_cnt[SS_SYMM_MAX_RANKS]; /* rank r's per-tile arrival counters (peer-mapped, zeroed) */
@@ -235,6 +237,10 @@ typedef struct ss_symm_group {
 
 /* bytes of each rank's signal region (2 x world vote slots + world done slots, uint64 each) */
 SS_API int ss_symm_signal_bytes(int32_t world, int64_t* bytes_host);
+/* layout check for FFI mirrors of ss_symm_group: byte offsets of its fields in
+   declaration order, then sizeof(ss_symm_group); *count_host = entries written
+   (fails with SS_ERR_CONFIG when cap is too small) */
+SS_API int ss_symm_group_layout(int64_t* offsets_host, int32_t cap, int32_t* count_host);
 
 /* C2 (and optionally C1) as one launch after the update kernel:
      exchange = 1: P2P flag exchange -- the N-bit OR of runtime.py:319-333 as a

@@ -140,6 +140,7 @@ _SIGS = {
     "ss_mean_f32": ([POINTER(c_void_p), c_int32, c_int64, _P, _P], c_int),
     "ss_replica_flag_max_i32": ([POINTER(c_void_p), c_int32, _P], c_int),
     "ss_symm_signal_bytes": ([c_int32, POINTER(c_int64)], c_int),
+    "ss_symm_group_layout": ([POINTER(c_int64), c_int32, POINTER(c_int32)], c_int),
     "ss_symm_sync_f32": ([POINTER(SymmGroupC), c_int64, _P, c_int32, c_float, _P, _P], c_int),
     "ss_step_symm_ga_f32": (
         [_P, _P, _P, c_int64, c_float, c_float, c_float, c_float, c_int32, c_int32,

@@ -28,6 +28,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <cstdlib>
 
@@ -153,6 +154,27 @@ int launch_symm(const SymmArgs& a, cudaStream_t s) {
 }  // namespace
 
 extern "C" {
+
+int ss_symm_group_layout(int64_t* offsets, int32_t cap, int32_t* count) {
+    const int64_t o[] = {
+        (int64_t)offsetof(ss_symm_group, bufs),        (int64_t)offsetof(ss_symm_group, pads),
+        (int64_t)offsetof(ss_symm_group, mc),          (int64_t)offsetof(ss_symm_group, seq),
+        (int64_t)offsetof(ss_symm_group, agreed_ring), (int64_t)offsetof(ss_symm_group, err),
+        (int64_t)offsetof(ss_symm_group, timeout_s),   (int64_t)offsetof(ss_symm_group, rank),
+        (int64_t)offsetof(ss_symm_group, world),       (int64_t)offsetof(ss_symm_group, ring_cap),
+        (int64_t)offsetof(ss_symm_group, reserved),    (int64_t)offsetof(ss_symm_group, order_mode),
+        (int64_t)offsetof(ss_symm_group, order_threshold), (int64_t)offsetof(ss_symm_group, tile_cnt),
+        (int64_t)offsetof(ss_symm_group, epoch),       (int64_t)offsetof(ss_symm_group, predictor),
+        (int64_t)offsetof(ss_symm_group, tile_elems),  (int64_t)offsetof(ss_symm_group, n_tiles),
+        (int64_t)offsetof(ss_symm_group, tile_norm),   (int64_t)offsetof(ss_symm_group, debug_events),
+        (int64_t)offsetof(ss_symm_group, debug_cap),   (int64_t)sizeof(ss_symm_group)};
+    const int32_t n = static_cast<int32_t>(sizeof(o) / sizeof(o[0]));
+    if (!offsets || !count) return fail(SS_ERR_CONFIG, "null argument");
+    if (cap < n) return fail(SS_ERR_CONFIG, "layout needs %d entries, got room for %d", n, cap);
+    for (int32_t i = 0; i < n; ++i) offsets[i] = o[i];
+    *count = n;
+    return SS_OK;
+}
 
 int ss_symm_signal_bytes(int32_t world, int64_t* bytes) {
     if (!bytes) return fail(SS_ERR_CONFIG, "null output");

@@ -42,6 +42,23 @@ def test_struct_layouts():
     assert N.workspace_bytes() > 8 * 148
 
 
+def test_symm_group_layout_matches_ctypes_mirror():
+    """Every field offset of ss_symm_group (and its size) as compiled into the
+    library equals the ctypes mirror the package passes to the step kernels."""
+    from paper_2307_07950_b200 import _native as N
+
+    cap = 64
+    offs = (ctypes.c_int64 * cap)()
+    count = ctypes.c_int32(0)
+    N.check(N.LIB.ss_symm_group_layout(offs, cap, ctypes.byref(count)))
+    names = [f[0] for f in N.SymmGroupC._fields_]
+    assert count.value == len(names) + 1
+    want = [getattr(N.SymmGroupC, n).offset for n in names] + [ctypes.sizeof(N.SymmGroupC)]
+    assert list(offs[: count.value]) == want
+    with pytest.raises(N.ConfigError):
+        N.check(N.LIB.ss_symm_group_layout(offs, 3, ctypes.byref(count)))
+
+
 def test_error_codes_map_to_reference_exceptions():
     from paper_2307_07950_b200 import _native as N
     from paper_2307_07950_b200.errors import ConfigError, SignalError
