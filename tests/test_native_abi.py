@@ -73,6 +73,20 @@ def test_error_codes_map_to_reference_exceptions():
         N.check(N.LIB.ss_norm_sq_f32(None, 10, None, None, None))
     with pytest.raises(ConfigError):
         N.check(N.LIB.ss_sgd_update_f32(None, None, None, -1, 0.1, 0, 0, 0, 0, 0, None, 1.0, None))
+    # the known-sync predicate validates like decide (DeltaThreshold rules)
+    st = N.SignalStateC()
+    st.smoothing, st.warmup = 0.5, 3
+    known = ctypes.c_int32(-1)
+    with pytest.raises(SignalError):
+        N.check(N.LIB.ss_sync_known_ahead(ctypes.byref(st), float("nan"), ctypes.byref(known)))
+    with pytest.raises(ConfigError):
+        N.check(N.LIB.ss_sync_known_ahead(None, 0.1, ctypes.byref(known)))
+    N.check(N.LIB.ss_sync_known_ahead(ctypes.byref(st), 0.1, ctypes.byref(known)))
+    assert known.value == 1  # step_count 0 < warmup
+    # the one-launch step rejects a missing group before any launch
+    with pytest.raises(ConfigError):
+        N.check(N.LIB.ss_step_symm_f32(None, None, None, 0, 0.1, 0, 0, 0, 0, 0, ctypes.byref(st), 0.1,
+                                       None, None, 0, None, None, None))
 
 
 def test_build_flags_target_sm100a():
