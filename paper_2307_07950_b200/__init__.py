@@ -11,6 +11,8 @@ Reference API kept (same names and semantics, /root/reference/pkg/src/selsync):
   wire:    flag_word, or_words, any_flag (flag semantics)
   errors:  ConfigError, SignalError, ProtocolError, TransportError
 New:
+  sync_known_ahead  the decision after the next observation is sync whatever
+                    the norm (warmup, delta == 0): the known-sync pass
   SelSyncStep     one rank's step over flat fp32 buffers (NCCL across GPUs)
   ReplicaSelSync  N simulated workers on one GPU
   FlatParameters  p.data / p.grad as views of flat buffers
@@ -26,6 +28,7 @@ from .signal import (  # noqa: F401
     observe,
     relative_change,
     replay_decisions,
+    sync_known_ahead,
 )
 from .config import AGG_MODES, SelSyncConfig  # noqa: F401
 from .data import (  # noqa: F401
