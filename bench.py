@@ -492,6 +492,10 @@ def main():
         ent = {"steps_per_s": world * args.steps / (m["ms"] / 1e3), "ms_per_step": m["ms"] / args.steps,
                "kernel_ms_mean": sum(m["kernel_ms"]) / len(m["kernel_ms"]) if m["kernel_ms"] else None}
         ent.update(exchange_stats(m, P, world))
+        ent["delta"] = 1e9 if name == "all_local" else 0.0
+        if name == "all_sync" and one_launch and args.order != "update_first":
+            ent["note"] = ("delta = 0: every step is sync before ||g||^2 is known, so the one-launch step "
+                           "takes the known-sync pass (no norm sweep, mean overlapped from the first tile)")
         line["modes"][name] = ent
     line.update({"exchange": exchange_stats(res, P, world)} if world > 1 else {})
     if one_launch and c2 is not None:
