@@ -135,6 +135,10 @@ SS_API int ss_norm_signal_f32(const float* g_dev, int64_t n, ss_signal_state* st
 /* K3: fused SGD (+momentum, +weight decay, optional Nesterov) in place:
      d = g + wd*w; m = first ? d : mu*m + (1-dampening)*d; d = nesterov ? d + mu*m : m;
      w = (w - lr*d) * s,  s = sync_scale if (sync_word_dev && *sync_word_dev & SS_FLAG_SYNC) else 1
+   When *sync_word_dev carries an error bit (>= 2: some rank observed a NaN or
+   negative norm) the kernel changes nothing: the NaN-safe order K1+K2 -> C1 ->
+   K3 leaves every rank's w and m as they were, like the reference, whose
+   observe raises (signal.py:67-68) before sgd_step runs (strategies.py:286, :383).
    With mu = wd = 0 this is sgd_step (model.py:215-221); s = 1/N pre-scales the
    parameters for an allreduce-SUM (the 1/N of aggregate_mean, strategies.py:167).
    m_dev may be NULL when momentum == 0. */
@@ -210,17 +214,26 @@ typedef struct ss_symm_group {
     int32_t rank;
     int32_t world;
     int32_t ring_cap;
-    int32_t reserved;
+    int32_t max_blocks;                 /* cap on the grid of the one-launch step kernels (0 = one full
+                                           wave: #SMs x resident blocks). Ranks that share ONE device
+                                           (colocated ranks) split it: every rank's grid must be
+                                           co-resident with every other rank's at once. */
     /* order of the one-launch step (ss_step_symm_f32):
          0  update first: K13 (update + ||g||^2) then, on sync, the mean;
          1  norm first: K1, vote, then on sync ONE kernel that overlaps the update
             of each tile with the NVLink mean of tiles all ranks have finished
             (on local steps the plain update);
          2  adaptive: order 1 when the predicted sync probability >= threshold (EWMA of
-            the agreed decisions per context of the previous two).
+            the agreed decisions per context of the previous two);
+         3  NaN-safe: order 1 in which the updates wait for the agreed vote, so a
+            step on which any rank observed a NaN norm (signal.py:67-68, raised
+            before sgd_step at strategies.py:286 vs :383) changes no rank's
+            parameters or momentum (SignalError on every rank).
        Orders 1/2 with tile_norm also run the known-sync pass on steps whose
-       decision is sync before ||g||^2 is known (ss_sync_known_ahead).
-       All orders compute identical parameters. Order 1/2 needs the fields below. */
+       decision is sync before ||g||^2 is known (ss_sync_known_ahead); a rank
+       whose update tile holds a NaN poisons the mean of that tile on its owner,
+       so a NaN never reaches another rank's buffer.
+       All orders compute identical parameters. Orders 1-3 need the fields below. */
     int32_t order_mode;
     float order_threshold;
     uint32_t* tile_cnt[SS_SYMM_MAX_RANKS]; /* rank r's per-tile arrival counters (peer-mapped, zeroed) */
@@ -235,7 +248,8 @@ typedef struct ss_symm_group {
     int64_t debug_cap;                  /* tickets recorded (4 x uint64 each) */
 } ss_symm_group;
 
-/* bytes of each rank's signal region (2 x world vote slots + world done slots, uint64 each) */
+/* bytes of each rank's signal region (2 x world vote slots + world done slots + world
+   poison slots, uint64 each) */
 SS_API int ss_symm_signal_bytes(int32_t world, int64_t* bytes_host);
 /* layout check for FFI mirrors of ss_symm_group: byte offsets of its fields in
    declaration order, then sizeof(ss_symm_group); *count_host = entries written
@@ -257,12 +271,17 @@ SS_API int ss_symm_group_layout(int64_t* offsets_host, int32_t cap, int32_t* cou
 SS_API int ss_symm_sync_f32(const ss_symm_group* g_host, int64_t n, int32_t* word_dev,
                             int32_t exchange, float scale, void* ws_dev, void* stream);
 
-/* The whole SelSync step in ONE cooperative launch (strategies.py:378-394):
-   fused update + ||g||^2 (K13) -> signal step in the finishing block (K2) ->
-   its vote posted to every peer -> every block waits for the N votes (C1) ->
-   on sync, the mean written into every rank's buffer with the 1/N applied in
-   the epilogue (C2) -> end barrier. w_dev must be g_host->bufs[g_host->rank].
-   *word_dev ends as the agreed word; the trace row keeps the own vote. */
+/* The whole SelSync step in ONE host launch (strategies.py:378-394), issued
+   as a cooperative launch (cudaLaunchAttributeCooperative: the driver places
+   every block at once or fails the launch -- blocks wait on each other):
+   fused update + ||g||^2 (K13) -> signal step in the last block to finish
+   (K2) -> its vote posted to every peer -> that block waits for the N votes
+   (C1) and broadcasts the agreed word to the other blocks of the grid -> on
+   sync, the mean written into every rank's buffer with the 1/N applied in
+   the epilogue (C2) -> end barrier. (Orders 1-3: see order_mode.)
+   w_dev must be g_host->bufs[g_host->rank]. *word_dev ends as the agreed
+   word; the trace row keeps the own vote. SS_ERR_CONFIG when the grid
+   (max_blocks) cannot be co-resident. */
 SS_API int ss_step_symm_f32(float* w_dev, const float* g_dev, float* m_dev, int64_t n, float lr,
                             float momentum, float dampening, float weight_decay, int32_t nesterov,
                             int32_t first_step, ss_signal_state* st_dev, double delta,
@@ -274,12 +293,21 @@ SS_API int ss_step_symm_f32(float* w_dev, const float* g_dev, float* m_dev, int6
    the mean GRADIENT over ranks (tile by tile, NVLS / P2P) and the update with
    it; on local steps the update with the own gradient. g_dev must be
    g_host->bufs[g_host->rank] (the gradient lives in symmetric memory);
-   needs tile_cnt / epoch / tile_elems of the group. */
+   needs tile_cnt / epoch / tile_elems of the group. The vote precedes every
+   update here, so an agreed word with an error bit (a NaN on any rank)
+   leaves every rank's parameters and momentum untouched. Cooperative launch. */
 SS_API int ss_step_symm_ga_f32(float* w_dev, float* g_dev, float* m_dev, int64_t n, float lr,
                                float momentum, float dampening, float weight_decay, int32_t nesterov,
                                int32_t first_step, ss_signal_state* st_dev, double delta,
                                int32_t* word_dev, ss_trace_row* trace_dev, int32_t trace_cap,
                                const ss_symm_group* g_host, void* ws_dev, void* stream);
+
+/* Co-resident block capacity of this device for the one-launch step kernel
+   that ss_step_symm_f32 (grads = 0) or ss_step_symm_ga_f32 (grads = 1) would
+   launch for this group and these hyperparameters (#SMs x resident blocks).
+   Ranks sharing one device set max_blocks <= this / ranks. */
+SS_API int ss_step_symm_grid_limit(const ss_symm_group* g_host, int32_t momentum, int32_t nesterov,
+                                   int32_t grads, int32_t* blocks_out_host);
 
 #ifdef __cplusplus
 }

@@ -80,7 +80,7 @@ class SymmGroupC(Structure):
         ("rank", c_int32),
         ("world", c_int32),
         ("ring_cap", c_int32),
-        ("reserved", c_int32),
+        ("max_blocks", c_int32),
         ("order_mode", c_int32),
         ("order_threshold", c_float),
         ("tile_cnt", c_void_p * SYMM_MAX_RANKS),
@@ -147,6 +147,7 @@ _SIGS = {
          _P, c_double, _P, _P, c_int32, POINTER(SymmGroupC), _P, _P],
         c_int,
     ),
+    "ss_step_symm_grid_limit": ([POINTER(SymmGroupC), c_int32, c_int32, c_int32, POINTER(c_int32)], c_int),
     "ss_step_symm_f32": (
         [_P, _P, _P, c_int64, c_float, c_float, c_float, c_float, c_int32, c_int32,
          _P, c_double, _P, _P, c_int32, POINTER(SymmGroupC), _P, _P],

@@ -16,6 +16,7 @@ CPU tensors, which the world-size-2 CPU tests use.
 
 from __future__ import annotations
 
+import ctypes
 import os
 from typing import Optional
 
@@ -84,6 +85,10 @@ class RankGroup:
         self._call(dist.all_reduce, t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def make_symmetric(self, numel: int, device, **kw) -> "SymmetricParams":
+        """This rank's view of a symmetric parameter buffer (torch symmetric memory)."""
+        return SymmetricParams(numel, device, self, **kw)
+
     def barrier(self, device=None) -> None:
         if self.distributed:
             if self.backend == "nccl" and device is not None:
@@ -94,90 +99,65 @@ class RankGroup:
 
 SIGNAL_OFFSET = 8192  # our slots sit at the top of torch's 9216-byte signal pad
 
+ORDERS = {"update_first": 0, "norm_first": 1, "adaptive": 2, "nan_safe": 3}
 
-class SymmetricParams:
-    """Flat fp32 buffer in symmetric (peer-mapped) memory + the device-side
-    SelSync exchange kernel ``ss_symm_sync_f32`` over it.
 
-    Allocation and address exchange use torch.distributed._symmetric_memory
-    (plumbing); the data path is our kernel: optional P2P flag exchange, then
-    -- only when the agreed flag word says sync -- the parameter mean written
-    into every rank's buffer (NVLS multimem when the switch supports it, P2P
-    loads/stores otherwise), with no host involvement.
-    """
+def default_tile_elems(numel: int) -> int:
+    # measured (N = 2, one graph replay per step): 4096-element tiles win
+    # below ~2M parameters (more tiles than blocks), 16384 from 4M up
+    return 4096 if numel <= (1 << 21) else 16384
 
-    ORDERS = {"update_first": 0, "norm_first": 1, "adaptive": 2}
 
-    def __init__(self, numel: int, device, comm: RankGroup, *, ring_capacity: int = 1 << 14,
-                 timeout_s: float = 30.0, use_multicast="auto", order: str = "update_first",
-                 order_threshold: float = 0.2, tile_elems: Optional[int] = None):
-        import ctypes
+class SymmetricView:
+    """One rank's view of a symmetric (peer-addressable) flat fp32 buffer and
+    of the per-rank device state the exchange kernels need, packed into the
+    C struct ``ss_symm_group``. Subclasses provide the peer addresses: torch
+    symmetric memory across GPUs (:class:`SymmetricParams`) or same-device
+    buffers of ranks that share one GPU (``colocated.ColocatedSymmetric``)."""
 
-        import torch.distributed._symmetric_memory as symm_mem
+    ORDERS = ORDERS
 
+    def _fill_group(self, *, numel: int, rank: int, world: int, bufs, pads, mc, tile_cnt,
+                    ring_capacity: int, timeout_s: float, order: str, order_threshold: float,
+                    tile_elems: int, max_blocks: int = 0) -> None:
         from . import _native as N
 
-        if not dist.is_initialized():
-            raise ConfigError("symmetric memory needs an initialised process group")
-        self.device = torch.device(device)
-        self.comm = comm
-        group = comm.group if comm.group is not None else dist.group.WORLD
-        self.buf = symm_mem.empty(numel, dtype=torch.float32, device=self.device)
-        self.hdl = symm_mem.rendezvous(self.buf, group)
-        self.world = int(self.hdl.world_size)
-        self.rank = int(self.hdl.rank)
-        need = ctypes.c_int64(0)
-        N.check(N.LIB.ss_symm_signal_bytes(self.world, ctypes.byref(need)))
-        if SIGNAL_OFFSET + need.value > int(self.hdl.signal_pad_size):
-            raise ConfigError("signal pad too small for the exchange slots")
-        if self.world > N.SYMM_MAX_RANKS:
+        if world > N.SYMM_MAX_RANKS:
             raise ConfigError(f"at most {N.SYMM_MAX_RANKS} ranks per symmetric group")
-        # NVLS moves 4P(1 + 1/N) bytes per link direction, the P2P two-shot
-        # 2(N-1)/N * 4P: multicast wins from N = 4 up (measured on B200:
-        # N=2 P2P 603 us vs NVLS 1030 us; N=4 NVLS 897 us vs P2P 920 us at 400 MB)
-        if use_multicast == "auto":
-            use_multicast = self.world >= 4
-        mc = int(self.hdl.multicast_ptr) if use_multicast else 0
+        if order not in ORDERS:
+            raise ConfigError(f"order must be one of {sorted(ORDERS)}, got {order!r}")
+        if tile_elems <= 0 or tile_elems % 4:
+            raise ConfigError("tile_elems must be a positive multiple of 4")
+        if max_blocks < 0:
+            raise ConfigError(f"max_blocks must be >= 0, got {max_blocks}")
+        self.rank, self.world = int(rank), int(world)
         self.multicast = bool(mc)
         self.mc = mc or None
-        # our slots of the local pad start zeroed; everyone zeroes before anyone posts
-        pad = self.hdl.get_signal_pad(self.rank, [need.value // 8], torch.int64, SIGNAL_OFFSET // 8)
-        pad.zero_()
         self.seq = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.ring_capacity = int(ring_capacity)
         self.agreed = torch.zeros(self.ring_capacity, dtype=torch.int32, device=self.device)
         self.timeout_s = float(timeout_s)
+        self.order = order
+        self.n_tiles = (numel + tile_elems - 1) // tile_elems
         g = N.SymmGroupC()
-        for r, p in enumerate(self.hdl.buffer_ptrs):
+        for r, p in enumerate(bufs):
             g.bufs[r] = int(p)
-        for r, p in enumerate(self.hdl.signal_pad_ptrs):
-            g.pads[r] = int(p) + SIGNAL_OFFSET
+        for r, p in enumerate(pads):
+            g.pads[r] = int(p)
+        for r, p in enumerate(tile_cnt):
+            g.tile_cnt[r] = int(p)
         g.mc = self.mc
         g.seq = self.seq.data_ptr()
         g.agreed_ring = self.agreed.data_ptr()
         g.err = self.err.data_ptr()
         g.timeout_s = self.timeout_s
         g.rank, g.world, g.ring_cap = self.rank, self.world, self.ring_capacity
+        g.max_blocks = int(max_blocks)
         # order of the one-launch step; the norm-first order overlaps the update
         # with the mean on sync steps and needs per-tile arrival counters
-        if order not in self.ORDERS:
-            raise ConfigError(f"order must be one of {sorted(self.ORDERS)}, got {order!r}")
-        if tile_elems is None:
-            # measured (N = 2, one graph replay per step): 4096-element tiles win
-            # below ~2M parameters (more tiles than blocks), 16384 from 4M up
-            tile_elems = 4096 if numel <= (1 << 21) else 16384
-        if tile_elems <= 0 or tile_elems % 4:
-            raise ConfigError("tile_elems must be a positive multiple of 4")
-        self.order = order
-        g.order_mode = self.ORDERS[order]
+        g.order_mode = ORDERS[order]
         g.order_threshold = float(order_threshold)
-        self.n_tiles = (numel + tile_elems - 1) // tile_elems
-        self.cnt = symm_mem.empty(max(1, self.n_tiles), dtype=torch.int32, device=self.device)
-        self.cnt_hdl = symm_mem.rendezvous(self.cnt, group)
-        self.cnt.zero_()
-        for r, p in enumerate(self.cnt_hdl.buffer_ptrs):
-            g.tile_cnt[r] = int(p)
         # known-sync pass (warmup steps, delta == 0): ||g||^2 partial per update
         # tile; SS_KNOWN_SYNC=0 disables the pass (A/B knob)
         self.tile_norm = None
@@ -191,11 +171,8 @@ class SymmetricParams:
         g.predictor = self.predictor.data_ptr()
         g.tile_elems = int(tile_elems)
         g.n_tiles = int(self.n_tiles)
-
         self.group_c = g
         self.group_ref = ctypes.byref(g)
-        torch.cuda.synchronize(self.device)
-        comm.barrier(self.device)
 
     def sync_(self, word: torch.Tensor, ws_ptr: int, *, exchange: bool, stream: int) -> None:
         from . import _native as N
@@ -221,3 +198,58 @@ class SymmetricParams:
         if int(self.err.item()) != 0:
             raise TransportError("a peer did not answer the device-side exchange within "
                                  f"{self.timeout_s:.0f} s")
+
+
+class SymmetricParams(SymmetricView):
+    """Flat fp32 buffer in symmetric (peer-mapped) memory + the device-side
+    SelSync exchange kernels over it.
+
+    Allocation and address exchange use torch.distributed._symmetric_memory
+    (plumbing); the data path is our kernels: optional P2P flag exchange, then
+    -- only when the agreed flag word says sync -- the parameter mean written
+    into every rank's buffer (NVLS multimem when the switch supports it, P2P
+    loads/stores otherwise), with no host involvement.
+    """
+
+    def __init__(self, numel: int, device, comm: RankGroup, *, ring_capacity: int = 1 << 14,
+                 timeout_s: float = 30.0, use_multicast="auto", order: str = "update_first",
+                 order_threshold: float = 0.2, tile_elems: Optional[int] = None, max_blocks: int = 0):
+        import torch.distributed._symmetric_memory as symm_mem
+
+        from . import _native as N
+
+        if not dist.is_initialized():
+            raise ConfigError("symmetric memory needs an initialised process group")
+        self.device = torch.device(device)
+        self.comm = comm
+        group = comm.group if comm.group is not None else dist.group.WORLD
+        self.buf = symm_mem.empty(numel, dtype=torch.float32, device=self.device)
+        self.hdl = symm_mem.rendezvous(self.buf, group)
+        world = int(self.hdl.world_size)
+        rank = int(self.hdl.rank)
+        need = ctypes.c_int64(0)
+        N.check(N.LIB.ss_symm_signal_bytes(world, ctypes.byref(need)))
+        if SIGNAL_OFFSET + need.value > int(self.hdl.signal_pad_size):
+            raise ConfigError("signal pad too small for the exchange slots")
+        # NVLS moves 4P(1 + 1/N) bytes per link direction, the P2P two-shot
+        # 2(N-1)/N * 4P: multicast wins from N = 4 up (measured on B200:
+        # N=2 P2P 603 us vs NVLS 1030 us; N=4 NVLS 897 us vs P2P 920 us at 400 MB)
+        if use_multicast == "auto":
+            use_multicast = world >= 4
+        mc = int(self.hdl.multicast_ptr) if use_multicast else 0
+        # our slots of the local pad start zeroed; everyone zeroes before anyone posts
+        pad = self.hdl.get_signal_pad(rank, [need.value // 8], torch.int64, SIGNAL_OFFSET // 8)
+        pad.zero_()
+        if tile_elems is None:
+            tile_elems = default_tile_elems(numel)
+        n_tiles = (numel + max(int(tile_elems), 1) - 1) // max(int(tile_elems), 1)
+        self.cnt = symm_mem.empty(max(1, n_tiles), dtype=torch.int32, device=self.device)
+        self.cnt_hdl = symm_mem.rendezvous(self.cnt, group)
+        self.cnt.zero_()
+        self._fill_group(numel=numel, rank=rank, world=world, bufs=self.hdl.buffer_ptrs,
+                         pads=[int(p) + SIGNAL_OFFSET for p in self.hdl.signal_pad_ptrs], mc=mc,
+                         tile_cnt=self.cnt_hdl.buffer_ptrs, ring_capacity=ring_capacity,
+                         timeout_s=timeout_s, order=order, order_threshold=order_threshold,
+                         tile_elems=int(tile_elems), max_blocks=max_blocks)
+        torch.cuda.synchronize(self.device)
+        comm.barrier(self.device)

@@ -1,0 +1,250 @@
+"""SelSync ranks that share ONE device: the multi-rank step kernels on one GPU.
+
+Across GPUs each rank's parameters live in torch symmetric memory and the
+one-launch step (``ss_step_symm_f32`` / ``ss_step_symm_ga_f32``) reads and
+writes its peers' buffers over NVLink. Here the N ranks are N
+``SelSyncStep`` objects on one device: every rank owns its own flat buffers,
+signal slots, tile counters, step counter, predictor, agreed ring and
+workspace, and its "peers" are the other ranks' same-device allocations --
+exactly the ``ss_symm_group`` layout the kernels expect, with plain device
+addresses instead of peer mappings. Each rank launches on its own CUDA stream
+and the grids split the device (``max_blocks`` = co-resident capacity / N),
+so all N grids are resident at once and the vote exchange, the tile tickets,
+the mean and the end barrier run as they do across GPUs -- the W = 2 / 4 / 8
+P2P instantiations of the kernels, ranks ordered and synchronised only by the
+device-side protocol (seq-tagged votes, release/acquire counters).
+
+This is the reference's N-worker exchange (flag relay runtime.py:319-333,
+mean round runtime.py:275-294 -> strategies.py:159-168, bootstrap
+runtime.py:178-191) through the same kernels a multi-GPU run uses, which a
+single-GPU box can run and check against the reference's golden traces.
+(The NVLS multicast path needs a multicast object over several GPUs and is
+not reachable this way.)
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import torch
+
+from . import _native as N
+from .collectives import SymmetricView, default_tile_elems
+from .config import SelSyncConfig
+from .errors import ConfigError
+
+
+class ColocatedWorld:
+    """Shared allocations of ``world`` ranks on one device: the N parameter
+    (or gradient) buffers, the N signal regions and the N tile-counter arrays
+    every rank's ``ss_symm_group`` points into."""
+
+    def __init__(self, world: int, device, *, max_blocks: Optional[int] = None):
+        if world < 1 or world > N.SYMM_MAX_RANKS:
+            raise ConfigError(f"world must be in [1, {N.SYMM_MAX_RANKS}], got {world}")
+        self.world = int(world)
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise ConfigError("colocated ranks need a CUDA device (no CPU fallback)")
+        self.max_blocks = max_blocks
+        self.numel: Optional[int] = None
+        self.views: dict[int, "ColocatedSymmetric"] = {}
+        self.bcast: dict = {}
+
+    def _allocate(self, numel: int, tile_elems: int) -> None:
+        if self.numel is not None:
+            if (numel, tile_elems) != (self.numel, self.tile_elems):
+                raise ConfigError(f"every colocated rank needs the same buffer and tile size: "
+                                  f"{(numel, tile_elems)} vs {(self.numel, self.tile_elems)}")
+            return
+        need = ctypes.c_int64(0)
+        N.check(N.LIB.ss_symm_signal_bytes(self.world, ctypes.byref(need)))
+        self.numel, self.tile_elems = int(numel), int(tile_elems)
+        n_tiles = max(1, (numel + tile_elems - 1) // tile_elems)
+        self.bufs = [torch.empty(numel, dtype=torch.float32, device=self.device) for _ in range(self.world)]
+        self.pads = torch.zeros(self.world, need.value // 8, dtype=torch.int64, device=self.device)
+        self.cnt = torch.zeros(self.world, n_tiles, dtype=torch.int32, device=self.device)
+
+    def group(self, rank: int) -> "ColocatedGroup":
+        if not 0 <= rank < self.world:
+            raise ConfigError(f"rank {rank} out of range for {self.world} colocated ranks")
+        return ColocatedGroup(self, rank)
+
+
+class ColocatedGroup:
+    """The ``RankGroup`` of one colocated rank. Votes and means travel inside
+    the one-launch step kernels; there is no NCCL communicator, so only the
+    symmetric-memory back end with the fused exchange is available."""
+
+    backend = "colocated"
+
+    def __init__(self, world: ColocatedWorld, rank: int):
+        self.world_obj = world
+        self.group = None
+        self.size = world.world
+        self.rank = int(rank)
+
+    @property
+    def distributed(self) -> bool:
+        return self.size > 1
+
+    def _no_host_collective(self, what: str):
+        raise ConfigError(f"colocated ranks have no host collective ({what}); use collective='symm' "
+                          "with flag_exchange='fused'")
+
+    def agree(self, word: torch.Tensor) -> None:
+        self._no_host_collective("flag allreduce")
+
+    def average_(self, buf: torch.Tensor) -> None:
+        self._no_host_collective("allreduce")
+
+    def sum_(self, buf: torch.Tensor) -> None:
+        self._no_host_collective("allreduce")
+
+    def broadcast_(self, buf: torch.Tensor, src_rank: int = 0) -> None:
+        """Bootstrap (runtime.py:178-191): every rank calls it with its own
+        tensor of the same role (ranks are constructed in order); the source
+        rank's call registers its tensor, the others copy it."""
+        key = (src_rank, buf.numel(), buf.dtype)
+        if self.rank == src_rank:
+            self.world_obj.bcast[key] = buf
+            return
+        src = self.world_obj.bcast.get(key)
+        if src is None:
+            raise ConfigError(f"rank {src_rank} must broadcast before rank {self.rank} receives")
+        buf.copy_(src)
+
+    def max_float(self, value: float, device) -> float:
+        return float(value)
+
+    def barrier(self, device=None) -> None:
+        pass
+
+    def make_symmetric(self, numel: int, device, **kw) -> "ColocatedSymmetric":
+        return ColocatedSymmetric(self.world_obj, self.rank, numel, device, **kw)
+
+
+class ColocatedSymmetric(SymmetricView):
+    """Rank ``rank``'s ``ss_symm_group`` over the shared same-device buffers."""
+
+    def __init__(self, world: ColocatedWorld, rank: int, numel: int, device, *, ring_capacity: int = 1 << 14,
+                 timeout_s: float = 10.0, use_multicast=False, order: str = "update_first",
+                 order_threshold: float = 0.2, tile_elems: Optional[int] = None, max_blocks: int = 0):
+        if use_multicast is True:
+            raise ConfigError("colocated ranks have no multicast object (NVLS needs several GPUs)")
+        self.device = torch.device(device)
+        if self.device != world.device:
+            raise ConfigError(f"rank on {self.device}, colocated world on {world.device}")
+        if rank in world.views:
+            raise ConfigError(f"colocated rank {rank} already has a symmetric buffer")
+        if tile_elems is None:
+            tile_elems = default_tile_elems(numel)
+        world._allocate(int(numel), int(tile_elems))
+        self.buf = world.bufs[rank]
+        self._fill_group(numel=numel, rank=rank, world=world.world, bufs=[b.data_ptr() for b in world.bufs],
+                         pads=[world.pads[r].data_ptr() for r in range(world.world)], mc=0,
+                         tile_cnt=[world.cnt[r].data_ptr() for r in range(world.world)],
+                         ring_capacity=ring_capacity, timeout_s=timeout_s, order=order,
+                         order_threshold=order_threshold, tile_elems=int(tile_elems),
+                         max_blocks=max_blocks or (world.max_blocks or 0))
+        world.views[rank] = self
+
+    def grid_limit(self, *, momentum: bool, nesterov: bool, grads: bool) -> int:
+        out = ctypes.c_int32(0)
+        N.check(N.LIB.ss_step_symm_grid_limit(self.group_ref, int(momentum), int(nesterov), int(grads),
+                                              ctypes.byref(out)))
+        return int(out.value)
+
+
+class ColocatedSelSync:
+    """N SelSync ranks on one GPU, each a :class:`SelSyncStep` over the
+    one-launch symmetric-memory step kernels, each on its own CUDA stream.
+
+    API as :class:`ReplicaSelSync` (``set_grads`` / ``step`` / ``decisions`` /
+    ``trace`` / ``params``), but every step is the multi-rank kernel itself:
+    ``step(lr)`` enqueues the N launches and returns; ``synchronize()`` waits
+    and raises ``SignalError`` / ``TransportError`` as ``SelSyncStep`` does.
+    """
+
+    def __init__(self, init_params: torch.Tensor, n_ranks: int, config: SelSyncConfig, *,
+                 order: str = "adaptive", order_threshold: float = 0.2, tile_elems: Optional[int] = None,
+                 timeout_s: float = 10.0, max_blocks: Optional[int] = None, trace_capacity: int = 4096,
+                 nan_safe: bool = False):
+        from .step import SelSyncStep
+
+        if not isinstance(init_params, torch.Tensor) or not init_params.is_cuda:
+            raise ConfigError("init_params must be a CUDA tensor")
+        if n_ranks not in (1, 2, 4, 8):
+            raise ConfigError(f"colocated ranks use the P2P widths 1, 2, 4, 8 of the step kernel, got {n_ranks}")
+        p0 = init_params.reshape(-1).to(torch.float32)
+        self.n = int(n_ranks)
+        self.device = p0.device
+        self.config = config
+        self.world = ColocatedWorld(self.n, self.device, max_blocks=max_blocks)
+        self.streams = [torch.cuda.Stream(self.device) for _ in range(self.n)]
+        self.ranks: list = []
+        for r in range(self.n):
+            # only rank 0 holds the init; the others start from garbage and must
+            # be overwritten by the bootstrap broadcast (runtime.py:178-191)
+            init = p0.clone() if r == 0 else torch.full_like(p0, 7.0)
+            st = SelSyncStep(init, torch.zeros_like(p0), config, group=self.world.group(r), collective="symm",
+                             flag_exchange="fused", order=order, order_threshold=order_threshold,
+                             tile_elems=tile_elems, timeout_s=timeout_s, trace_capacity=trace_capacity,
+                             nan_safe=nan_safe)
+            self.ranks.append(st)
+        if max_blocks is None:
+            cap = self.ranks[0].symm.grid_limit(momentum=config.momentum != 0.0, nesterov=config.nesterov,
+                                               grads=config.aggregation == "grads")
+            per = cap // self.n
+            if per < 1:
+                raise ConfigError(f"{self.n} colocated grids do not fit on this device ({cap} resident blocks)")
+            max_blocks = per
+        for st in self.ranks:
+            st.symm.group_c.max_blocks = int(max_blocks)
+        self.max_blocks = int(max_blocks)
+        torch.cuda.synchronize(self.device)
+
+    @property
+    def params(self) -> list:
+        return [st.params for st in self.ranks]
+
+    @property
+    def grads(self) -> list:
+        return [st.grads for st in self.ranks]
+
+    def set_grads(self, grads: Sequence[torch.Tensor]) -> None:
+        """Copy each rank's gradient on that rank's stream (ordered after its
+        previous step, as a backward on the rank's own GPU would be)."""
+        cur = torch.cuda.current_stream(self.device)
+        for st, s, g in zip(self.ranks, self.streams, grads):
+            s.wait_stream(cur)  # g may still be in flight on the caller's stream
+            with torch.cuda.stream(s):
+                st.grads.copy_(g.reshape(-1), non_blocking=True)
+            g.record_stream(s)
+
+    def step(self, lr: float) -> None:
+        """Enqueue one step on every rank (N launches, no host round-trip)."""
+        for st, s in zip(self.ranks, self.streams):
+            with torch.cuda.stream(s):
+                st.step_async(lr)
+
+    def synchronize(self) -> None:
+        for s in self.streams:
+            s.synchronize()
+        for st, s in zip(self.ranks, self.streams):
+            with torch.cuda.stream(s):
+                st.synchronize()
+
+    @property
+    def steps_done(self) -> int:
+        return self.ranks[0].steps_done
+
+    def decisions(self, rank: int = 0) -> list:
+        return self.ranks[rank].decisions()
+
+    def trace(self, rank: int):
+        return self.ranks[rank].signal.read_trace()
+
+    def records(self) -> list:
+        return [row for st in self.ranks for row in st.records()]

@@ -35,7 +35,8 @@ __host__ __device__ inline Workspace ws_view(void* ws) {
     return Workspace{reinterpret_cast<unsigned int*>(b), reinterpret_cast<double*>(b + kWsHeader)};
 }
 // header: norm arrival counter at 0, exchange arrival counter at 64, ticket at
-// 128, the update-first step's decision broadcast at 192; then the partials
+// 128, the update-first step's decision broadcast at 192, the one-launch
+// step's block-start counter at 224; then the partials
 constexpr int64_t kWsBytes = kWsHeader + 8 * kMaxGrid;
 
 // ------------------------------------------- exact IEEE scalar arithmetic
@@ -124,12 +125,15 @@ __host__ __device__ inline int vote_core(const ss_signal_state* s, double delta)
 }
 
 // The decision after the NEXT observation is sync whatever the observed norm
-// (finite, >= 0): the observation about to be made is number <= warmup, or
-// delta == 0 (Delta >= 0 whenever it is defined, inf included). Sound and
-// complete: past warmup with delta > 0, observing x == ewma_current gives
-// Delta == 0 < delta (local). tests/test_signal_api.py checks both directions.
-__host__ __device__ inline bool sync_known_ahead_core(int64_t step_count, int32_t warmup, double delta) {
-    return delta == 0.0 || step_count + 1 <= static_cast<int64_t>(warmup);
+// (>= 0, not NaN): the observation about to be made is number <= warmup, or
+// delta == 0 with a finite ewma_current (then Delta >= 0, inf included; an
+// infinite EWMA would give Delta = inf/inf = NaN, i.e. "local"). Sound and
+// complete: otherwise observing x == ewma_current gives Delta == 0 < delta,
+// or NaN (local). tests/test_signal_api.py checks both directions.
+__host__ __device__ inline bool sync_known_ahead_core(int64_t step_count, int32_t warmup, double delta,
+                                                      double ewma_current) {
+    if (step_count + 1 <= static_cast<int64_t>(warmup)) return true;
+    return delta == 0.0 && ewma_current - ewma_current == 0.0;  // finite
 }
 
 // K2 body: one thread. Writes the flag word and the trace row.
@@ -319,7 +323,13 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     float s = 1.0f;
-    if (a.sync_word != nullptr && (__ldg(a.sync_word) & SS_FLAG_SYNC)) s = a.sync_scale;
+    if (a.sync_word != nullptr) {
+        const int word = __ldg(a.sync_word);
+        // an error bit anywhere (NaN / negative norm on some rank): change nothing,
+        // as the reference raises in observe before sgd_step (strategies.py:286, :383)
+        if (word & ~SS_FLAG_SYNC) return 0.0;
+        if (word & SS_FLAG_SYNC) s = a.sync_scale;
+    }
     double acc = 0.0;
     float mdummy = 0.0f;
     for (int64_t i = tid; i < a.head; i += stride) {
@@ -335,6 +345,32 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
     float* mb = MOM ? a.m + a.head : nullptr;
     const int64_t nvec = (a.n - a.head) >> 2;
     int64_t i = tid;
+    if constexpr (U == 1) {
+        // pointer-bumped loop with a 32-bit trip count: fewer live 64-bit
+        // values than index arithmetic (keeps the 3-stream momentum pass in
+        // 64 registers without spills at 4 blocks x 256 threads per SM)
+        if (i < nvec) {
+            const int iters = static_cast<int>((nvec - 1 - i) / stride) + 1;
+            const int64_t step = 4 * stride;
+            const float* pg = gb + 4 * i;
+            float* pw = wb + 4 * i;
+            float* pm = MOM ? mb + 4 * i : nullptr;
+            for (int it = 0; it < iters; ++it) {
+                float4 gv = ld_pol_ro<CP>(pg), wv = ld_pol<CP>(pw);
+                float4 mm = MOM ? ld_pol<CP>(pm) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (NORM) acc = sq4(gv, acc);
+                sgd_elem<MOM, NEST>(wv.x, gv.x, mm.x, a, s);
+                sgd_elem<MOM, NEST>(wv.y, gv.y, mm.y, a, s);
+                sgd_elem<MOM, NEST>(wv.z, gv.z, mm.z, a, s);
+                sgd_elem<MOM, NEST>(wv.w, gv.w, mm.w, a, s);
+                st_pol<CP>(pw, wv);
+                if (MOM) st_pol<CP>(pm, mm);
+                pg += step;
+                pw += step;
+                if (MOM) pm += step;
+            }
+        }
+    } else
     for (; i + (U - 1) * stride < nvec; i += U * stride) {
         float4 gv[U], wv[U], mv[U];
 #pragma unroll
@@ -357,17 +393,19 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
             if (MOM) st_pol<CP>(mb + k, mm);
         }
     }
-    for (; i < nvec; i += stride) {
-        const int64_t k = 4 * i;
-        float4 gv = ld_cs4(gb + k), wv = ld_cs4(wb + k);
-        float4 mm = MOM ? ld_cs4(mb + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (NORM) acc = sq4(gv, acc);
-        sgd_elem<MOM, NEST>(wv.x, gv.x, mm.x, a, s);
-        sgd_elem<MOM, NEST>(wv.y, gv.y, mm.y, a, s);
-        sgd_elem<MOM, NEST>(wv.z, gv.z, mm.z, a, s);
-        sgd_elem<MOM, NEST>(wv.w, gv.w, mm.w, a, s);
-        st_cs4(wb + k, wv);
-        if (MOM) st_cs4(mb + k, mm);
+    if constexpr (U > 1) {  // with U == 1 the loop above covers every vector
+        for (; i < nvec; i += stride) {
+            const int64_t k = 4 * i;
+            float4 gv = ld_cs4(gb + k), wv = ld_cs4(wb + k);
+            float4 mm = MOM ? ld_cs4(mb + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (NORM) acc = sq4(gv, acc);
+            sgd_elem<MOM, NEST>(wv.x, gv.x, mm.x, a, s);
+            sgd_elem<MOM, NEST>(wv.y, gv.y, mm.y, a, s);
+            sgd_elem<MOM, NEST>(wv.z, gv.z, mm.z, a, s);
+            sgd_elem<MOM, NEST>(wv.w, gv.w, mm.w, a, s);
+            st_cs4(wb + k, wv);
+            if (MOM) st_cs4(mb + k, mm);
+        }
     }
     for (int64_t j = a.head + 4 * nvec + tid; j < a.n; j += stride) {
         float w = a.w[j], g = a.g[j];

@@ -191,20 +191,10 @@ int launch_norm_u(const float* g, int64_t n, Finish f, void* stream, const char*
     return check_launch(what);
 }
 
-// SS_NORM_UNROLL overrides the K1 unroll for tuning sweeps
+// K1 unroll: 4 independent 16-byte loads in flight per thread (measured at
+// P = 100M: U = 4 6.29-6.42 TB/s, the best of 1 / 2 / 4 / 8)
 int launch_norm(const float* g, int64_t n, const Finish& f, void* stream, const char* what) {
-    static int u = -1;
-    if (u < 0) {
-        const char* e = getenv("SS_NORM_UNROLL");
-        u = e ? atoi(e) : 0;
-    }
-    switch (u) {
-        case 1: return launch_norm_u<1>(g, n, f, stream, what);
-        case 2: return launch_norm_u<2>(g, n, f, stream, what);
-        case 4: return launch_norm_u<4>(g, n, f, stream, what);
-        case 8: return launch_norm_u<8>(g, n, f, stream, what);
-        default: return launch_norm_u<kNormUnroll>(g, n, f, stream, what);
-    }
+    return launch_norm_u<kNormUnroll>(g, n, f, stream, what);
 }
 
 }  // namespace
@@ -283,7 +273,7 @@ int ss_sync_known_ahead(const ss_signal_state* st, double delta, int32_t* known_
     if (!st || !known_out) return fail(SS_ERR_CONFIG, "null argument");
     int rc = check_delta_impl(delta);
     if (rc) return rc;
-    *known_out = sync_known_ahead_core(st->step_count, st->warmup, delta) ? 1 : 0;
+    *known_out = sync_known_ahead_core(st->step_count, st->warmup, delta, st->ewma_current) ? 1 : 0;
     return SS_OK;
 }
 
@@ -403,41 +393,15 @@ int launch_sgd_v(const SgdArgs& a, const Finish& f0, void* stream) {
     return check_launch(NORM ? "ss_update_norm_signal_f32" : "ss_sgd_update_f32");
 }
 
-// SS_SGD_VARIANT="<cp><u>" (e.g. "21") overrides the cache policy / unroll of
-// the momentum K13 kernel for tuning sweeps (tools/sgd_sweep.py); unset = default
-// measured at P = 100M (tools/sgd_sweep.py): momentum (3 streams) U=1 6.40 TB/s vs U=2 5.92,
-// U=4 5.67; plain (2 streams) U=2 6.23 vs U=1 6.01
+// measured at P = 100M (round-1 sweep over unroll x cache policy): momentum
+// (3 streams) U=1 6.40 TB/s vs U=2 5.92, U=4 5.67; plain (2 streams) U=2 6.23
+// vs U=1 6.01; evict-first (.cs) loads/stores beat plain, L2::256B prefetch
+// and the non-coherent gradient path
 template <bool MOM>
 constexpr int kSgdUnroll = MOM ? 1 : 2;
 
-int sgd_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("SS_SGD_VARIANT");
-        v = e ? atoi(e) : 0;
-    }
-    return v;
-}
-
 template <bool MOM, bool NEST, bool NORM>
 int launch_sgd(const SgdArgs& a, const Finish& f0, void* stream) {
-    if constexpr (!NEST) {
-        switch (sgd_variant()) {
-            case 1: return launch_sgd_v<MOM, NEST, NORM, 1, 0>(a, f0, stream);
-            case 4: return launch_sgd_v<MOM, NEST, NORM, 4, 0>(a, f0, stream);
-            case 11: return launch_sgd_v<MOM, NEST, NORM, 1, 1>(a, f0, stream);
-            case 12: return launch_sgd_v<MOM, NEST, NORM, 2, 1>(a, f0, stream);
-            case 14: return launch_sgd_v<MOM, NEST, NORM, 4, 1>(a, f0, stream);
-            case 21: return launch_sgd_v<MOM, NEST, NORM, 1, 2>(a, f0, stream);
-            case 22: return launch_sgd_v<MOM, NEST, NORM, 2, 2>(a, f0, stream);
-            case 24: return launch_sgd_v<MOM, NEST, NORM, 4, 2>(a, f0, stream);
-            case 31: return launch_sgd_v<MOM, NEST, NORM, 1, 3>(a, f0, stream);
-            case 32: return launch_sgd_v<MOM, NEST, NORM, 2, 3>(a, f0, stream);
-            case 34: return launch_sgd_v<MOM, NEST, NORM, 4, 3>(a, f0, stream);
-            case 2: return launch_sgd_v<MOM, NEST, NORM, 2, 0>(a, f0, stream);
-            default: break;
-        }
-    }
     return launch_sgd_v<MOM, NEST, NORM, kSgdUnroll<MOM>, 0>(a, f0, stream);
 }
 

@@ -68,7 +68,11 @@ struct OverlapArgs {
     uint64_t* dbg;             // optional per-ticket timeline: {kind << 48 | tile, t0, t_ready, t_end}
     int64_t dbg_cap;
     double* tile_norm;         // known-sync pass: ||g||^2 partial per tile (NULL: pass disabled)
+    unsigned int* started;     // blocks that took this launch's order snapshot (workspace, self-resetting)
 };
+
+// order bits of one launch, decided once per block at kernel start
+constexpr int kNormFirst = 1, kKnown = 2, kSafe = 4;
 
 __device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -98,6 +102,30 @@ __device__ __forceinline__ void predictor_update(float* pr, int w) {
     const int s = w == SS_FLAG_SYNC ? 1 : 0;
     pr[h] = 0.75f * pr[h] + (s ? 0.25f : 0.0f);
     pr[4] = static_cast<float>(((h << 1) | s) & 3);
+}
+
+// bounded spin until *p >= want (gpu scope); sets the error word on timeout
+__device__ void wait_count_gpu(const unsigned int* p, unsigned int want, const SymmArgs& s) {
+    const uint64_t t0 = now_ns();
+    while (*reinterpret_cast<const volatile unsigned int*>(p) < want) {
+        if (now_ns() - t0 > s.timeout_ns) {
+            atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+            return;
+        }
+        __nanosleep(32);
+    }
+    __threadfence();
+}
+
+// a peer met a NaN in an update tile of this step (known-sync pass)
+__device__ bool poisoned(const SymmArgs& s, uint64_t seq) {
+    bool p = false;
+    for (int j = 0; j < s.world; ++j) p |= ld_acquire_sys(poison_slot(s, s.rank, j)) == seq;
+    return p;
+}
+
+__device__ void post_poison(const SymmArgs& s, uint64_t seq) {
+    for (int j = 0; j < s.world; ++j) st_release_sys(poison_slot(s, j, s.rank), seq);
 }
 
 // end of a sync step on this rank: done tags to every peer, wait for all
@@ -144,6 +172,9 @@ __device__ void known_tile_done(const Finish& f, const SymmArgs& s, const Overla
     v = block_sum(v);
     if (threadIdx.x == 0) {
         *ws.counter = 0u;
+        // K2 advances step_count, which every block reads once at kernel start
+        // to pick this launch's order: run it only after all of them have
+        wait_count_gpu(o.started, gridDim.x, s);
         signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
         const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
         __threadfence_system();
@@ -156,17 +187,34 @@ __device__ void known_tile_done(const Finish& f, const SymmArgs& s, const Overla
 // observation about to be made is number <= warmup, signal.py:105-106) or
 // delta == 0 (Delta >= 0 always). Same on every rank (same step count, delta).
 __device__ __forceinline__ bool sync_known_ahead(const Finish& f) {
-    if (f.delta == 0.0) return true;
     const volatile ss_signal_state* st = f.st;
-    return sync_known_ahead_core(st->step_count, st->warmup, f.delta);
+    return sync_known_ahead_core(st->step_count, st->warmup, f.delta, st->ewma_current);
+}
+
+// This launch's order, read by thread 0 of every block from state that only
+// the last block of the PREVIOUS launch (predictor) or a K2 that waits for
+// every block's arrival here (known pass) writes: all blocks agree.
+__device__ int order_snapshot(const Finish& f, const OverlapArgs& o) {
+    __shared__ int s_order;
+    if (threadIdx.x == 0) {
+        const bool known = (o.mode == 1 || o.mode == 2) && o.tile_norm != nullptr && sync_known_ahead(f);
+        const bool nf = known || o.mode == 1 || o.mode == 3 ||
+                        (o.mode == 2 && predicted_sync(o.predictor) >= o.threshold);
+        s_order = (nf ? kNormFirst : 0) | (known ? kKnown : 0) | (o.mode == 3 ? kSafe : 0);
+        __threadfence();  // the state reads above complete before the arrival below
+        atomicAdd(o.started, 1u);
+    }
+    __syncthreads();
+    return s_order;
 }
 
 template <bool MOM, bool NEST, int W>
 __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
-                                     uint64_t seq, bool known) {
+                                     uint64_t seq, bool known, bool safe) {
     __shared__ unsigned long long s_ticket;
     __shared__ int s_vote;
     __shared__ bool s_last;
+    __shared__ bool s_go;
     const int N = s.world;
     const int64_t T = o.n_tiles;
     const int64_t groups = (T + N - 1) / N + o.lag;
@@ -233,13 +281,27 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                 const int64_t t = grp * N + pos;
                 if (t < T) {
                     const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
-                    if (!known) {
+                    if (safe) {
+                        // NaN-safe order: no update before the agreed vote; an
+                        // error bit on any rank (or a timeout) skips every update
+                        if (threadIdx.x == 0 && s_vote == -2) s_vote = agreed_vote(s, seq);
+                        __syncthreads();
+                    }
+                    if (safe && (s_vote & ~SS_FLAG_SYNC) != 0) {
+                        // counted all the same: tile counts advance by N every norm-first step
+                    } else if (!known) {
                         sgd_block_range<MOM, NEST>(a, e0, e1);
                         __syncthreads();
                     } else {
                         // block_sum's barriers also order the block's stores
                         const double ts = block_sum(sgd_block_range<MOM, NEST, 1, false, true>(a, e0, e1));
-                        if (threadIdx.x == 0) o.tile_norm[t] = ts;
+                        if (threadIdx.x == 0) {
+                            o.tile_norm[t] = ts;
+                            // a NaN in this tile: no owner may average anything from
+                            // here on (the mean runs before the vote carries the error);
+                            // the tag is released before this tile's count below
+                            if (ts != ts) post_poison(s, seq);
+                        }
                     }
                     // release at sys scope: the block's stores (ordered by the
                     // barrier) are visible to the owner before the count
@@ -252,20 +314,27 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                 const int64_t m = grp - o.lag;
                 const int64_t t = m * N + s.rank;
                 if (m >= 0 && t < T) {
-                    if (threadIdx.x == 0 && s_vote == -2) s_vote = agreed_vote(s, seq);
-                    __syncthreads();
-                    if (s_vote == SS_FLAG_SYNC) {
-                        if (threadIdx.x == 0) {
+                    if (threadIdx.x == 0) {
+                        if (s_vote == -2) s_vote = agreed_vote(s, seq);
+                        bool go = s_vote == SS_FLAG_SYNC;
+                        if (go) {
                             const uint64_t t0 = now_ns();
                             while (static_cast<int32_t>(ld_acquire_sys_u32(o.cnt[s.rank] + t) - target) < 0) {
                                 if (now_ns() - t0 > s.timeout_ns) {
                                     atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+                                    go = false;
                                     break;
                                 }
                                 __nanosleep(128);
                             }
+                            // known pass: a NaN met by any rank before its count
+                            // of this tile stops the mean here (acquired above)
+                            if (go && known && poisoned(s, seq)) go = false;
                         }
-                        __syncthreads();
+                        s_go = go;
+                    }
+                    __syncthreads();
+                    if (s_go) {
                         if (rec) t_ready = now_ns();
                         const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
                         average_block_range<W>(s, e0, e1);
@@ -295,6 +364,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
         if (o.dbg) o.dbg[4 * o.dbg_cap + 5] = now_ns();
         *o.ticket = 0ull;
         *o.epoch = epoch;
+        *o.started = 0u;
         *s.arrive = 0u;
         *s.seq = static_cast<uint32_t>(seq);
     }
@@ -332,6 +402,7 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
         v = block_sum(v);
         if (threadIdx.x == 0) {
             *ws.counter = 0u;
+            *o.started = 0u;  // every block has arrived: all took their snapshot
             signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
             const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
             __threadfence_system();
@@ -348,6 +419,7 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
     } else if (threadIdx.x == 0) {
         bool to = false;
         const uint64_t t = wait_tag_gpu(decided, seq, s.timeout_ns, &to);
+        if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
         s_w = to ? -1 : static_cast<int>(static_cast<uint32_t>(t));
     }
     __syncthreads();
@@ -369,12 +441,11 @@ template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     // the order of this step: identical on every rank (same decision history)
-    const bool known = o.mode != 0 && o.tile_norm != nullptr && sync_known_ahead(f);
-    const bool norm_first = known || o.mode == 1 || (o.mode == 2 && predicted_sync(o.predictor) >= o.threshold);
+    const int order = order_snapshot(f, o);
     uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {start, vote posted, votes in, -, last arrival, end}
     if (mark && blockIdx.x == 0 && threadIdx.x == 0) mark[0] = now_ns();
-    if (norm_first) {
-        nf_body<MOM, NEST, W>(a, f, s, o, seq, known);
+    if (order & kNormFirst) {
+        nf_body<MOM, NEST, W>(a, f, s, o, seq, (order & kKnown) != 0, (order & kSafe) != 0);
         return;
     }
     uf_body<MOM, NEST, W>(a, f, s, o, seq);
@@ -431,6 +502,10 @@ __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish 
     if (threadIdx.x == 0) s_vote = agreed_vote(s, seq);
     __syncthreads();
     const bool sync = s_vote == SS_FLAG_SYNC;
+    // the vote precedes every update here: an error bit on any rank (or a
+    // timeout) leaves w and m untouched on every rank (strategies.py:286 raises
+    // before the deferred update of :395-399)
+    const bool skip = (s_vote & ~SS_FLAG_SYNC) != 0;
     unsigned long long nxt = 0;  // next ticket fetched ahead, as in nf_body
     if (threadIdx.x == 0) nxt = atomicAdd(o.ticket, 1ull);
     for (;;) {
@@ -468,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish 
                 }
                 __syncthreads();
                 const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
-                sgd_block_range<MOM, NEST, 2, true>(a, e0, e1);
+                if (!skip) sgd_block_range<MOM, NEST, 2, true>(a, e0, e1);
             }
         }
     }
@@ -494,47 +569,88 @@ int occupancy(K kernel, int threads) {
     return x;
 }
 
+// SS_COOP=0 drops the cooperative attribute (A/B timing of the attribute only)
+bool coop_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("SS_COOP");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// Grid of a one-launch step: one wave (#SMs x resident blocks, fewer for small
+// P), capped by the group's max_blocks (ranks sharing one device split it).
+int step_grid(int64_t vec_work, int per_thread, int resident, int max_blocks) {
+    int grid = static_cast<int>(grid_for(vec_work, per_thread, resident));
+    if (max_blocks > 0 && grid > max_blocks) grid = max_blocks;
+    return grid;
+}
+
+// The blocks of a step kernel wait on each other (decision broadcast, tile
+// tickets, the known pass's snapshot count), so the grid must be co-resident:
+// a cooperative launch makes the driver place every block at once or fail the
+// launch (cudaErrorCooperativeLaunchTooLarge -> SS_ERR_CONFIG) instead of
+// letting a partly placed grid spin into the timeout. Capturable in CUDA graphs.
+template <typename... P, typename... A>
+int launch_coop(void (*kernel)(P...), int grid, void* stream, const char* what, A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = coop_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return fail(e == cudaErrorCooperativeLaunchTooLarge ? SS_ERR_CONFIG : SS_ERR_CUDA,
+                    "%s: %s (grid %d of %d threads: every block must be co-resident)", what,
+                    cudaGetErrorString(e), grid, kThreads);
+    }
+    return check_launch(what);
+}
+
 template <bool MOM, bool NEST, int W>
-int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, void* stream) {
+int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, int max_blocks, void* stream) {
     static int res_step = 0;
     if (res_step == 0) res_step = occupancy(step_kernel<MOM, NEST, W>, kThreads);
-    // one wave (grid_for caps at #SMs x resident blocks): blocks wait on each
-    // other (decision broadcast, tickets), so every block must be co-resident
-    const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res_step));
+    const int grid = step_grid((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res_step, max_blocks);
     f.total_blocks = grid;
     // norm-first pass: the in-flight window is ~grid tickets = grid / (N + 1)
     // groups; the mean of a tile is scheduled one window after its update
     o.lag = grid / (sa.world + 1) + 2;
-    step_kernel<MOM, NEST, W><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, f, sa, o);
-    return check_launch("ss_step_symm_f32");
+    return launch_coop(step_kernel<MOM, NEST, W>, grid, stream, "ss_step_symm_f32", a, f, sa, o);
 }
 
 template <int W>
 int dispatch_step(const SgdArgs& a, const Finish& f, const SymmArgs& sa, const OverlapArgs& o, bool mom,
-                  bool nest, void* stream) {
-    if (!mom) return launch_step<false, false, W>(a, f, sa, o, stream);
-    if (nest) return launch_step<true, true, W>(a, f, sa, o, stream);
-    return launch_step<true, false, W>(a, f, sa, o, stream);
+                  bool nest, int max_blocks, void* stream) {
+    if (!mom) return launch_step<false, false, W>(a, f, sa, o, max_blocks, stream);
+    if (nest) return launch_step<true, true, W>(a, f, sa, o, max_blocks, stream);
+    return launch_step<true, false, W>(a, f, sa, o, max_blocks, stream);
 }
 
 
 template <bool MOM, bool NEST, int W>
-int launch_step_ga(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, void* stream) {
+int launch_step_ga(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, int max_blocks, void* stream) {
     static int res = 0;
     if (res == 0) res = occupancy(step_ga_kernel<MOM, NEST, W>, kThreads);
-    const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res));
+    const int grid = step_grid((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res, max_blocks);
     f.total_blocks = grid;
     o.lag = grid / (sa.world + 1) + 2;
-    step_ga_kernel<MOM, NEST, W><<<grid, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, f, sa, o);
-    return check_launch("ss_step_symm_ga_f32");
+    return launch_coop(step_ga_kernel<MOM, NEST, W>, grid, stream, "ss_step_symm_ga_f32", a, f, sa, o);
 }
 
 template <int W>
 int dispatch_step_ga(const SgdArgs& a, const Finish& f, const SymmArgs& sa, const OverlapArgs& o, bool mom,
-                     bool nest, void* stream) {
-    if (!mom) return launch_step_ga<false, false, W>(a, f, sa, o, stream);
-    if (nest) return launch_step_ga<true, true, W>(a, f, sa, o, stream);
-    return launch_step_ga<true, false, W>(a, f, sa, o, stream);
+                     bool nest, int max_blocks, void* stream) {
+    if (!mom) return launch_step_ga<false, false, W>(a, f, sa, o, max_blocks, stream);
+    if (nest) return launch_step_ga<true, true, W>(a, f, sa, o, max_blocks, stream);
+    return launch_step_ga<true, false, W>(a, f, sa, o, max_blocks, stream);
 }
 
 }  // namespace
@@ -562,7 +678,8 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
     o.dbg_cap = grp->debug_events ? grp->debug_cap : 0;
     o.mode = grp->order_mode;
     o.threshold = grp->order_threshold;
-    if (o.mode < 0 || o.mode > 2) return fail(SS_ERR_CONFIG, "order_mode must be 0, 1 or 2, got %d", o.mode);
+    o.started = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 224);
+    if (o.mode < 0 || o.mode > 3) return fail(SS_ERR_CONFIG, "order_mode must be 0, 1, 2 or 3, got %d", o.mode);
     if (o.mode != 0) {
         if (a.head != 0) return fail(SS_ERR_CONFIG, "norm-first order needs 16-byte aligned w, g, m");
         if (!grp->epoch || !grp->predictor || grp->tile_elems <= 0 || (grp->tile_elems & 3))
@@ -580,14 +697,16 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
         o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
         o.tile_norm = grp->tile_norm;
     }
+    if (grp->max_blocks < 0) return fail(SS_ERR_CONFIG, "max_blocks must be >= 0, got %d", grp->max_blocks);
+    const int mb = grp->max_blocks;
     Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
     const bool mom = momentum != 0.0f, nest = nesterov != 0;
     switch (symm_width(sa)) {
-        case 0: return dispatch_step<0>(a, f, sa, o, mom, nest, stream);
-        case 1: return dispatch_step<1>(a, f, sa, o, mom, nest, stream);  // single rank (profiling)
-        case 2: return dispatch_step<2>(a, f, sa, o, mom, nest, stream);
-        case 4: return dispatch_step<4>(a, f, sa, o, mom, nest, stream);
-        case 8: return dispatch_step<8>(a, f, sa, o, mom, nest, stream);
+        case 0: return dispatch_step<0>(a, f, sa, o, mom, nest, mb, stream);
+        case 1: return dispatch_step<1>(a, f, sa, o, mom, nest, mb, stream);  // single rank (profiling)
+        case 2: return dispatch_step<2>(a, f, sa, o, mom, nest, mb, stream);
+        case 4: return dispatch_step<4>(a, f, sa, o, mom, nest, mb, stream);
+        case 8: return dispatch_step<8>(a, f, sa, o, mom, nest, mb, stream);
         default:
             return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 1, 2, 4, 8)", sa.world);
     }
@@ -627,15 +746,54 @@ extern "C" int ss_step_symm_ga_f32(float* w, float* g, float* m, int64_t n, floa
     o.tile = grp->tile_elems;
     o.n_tiles = tiles;
     o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
+    o.started = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 224);
+    if (grp->max_blocks < 0) return fail(SS_ERR_CONFIG, "max_blocks must be >= 0, got %d", grp->max_blocks);
+    const int mb = grp->max_blocks;
     Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
     const bool mom = momentum != 0.0f, nest = nesterov != 0;
     switch (symm_width(sa)) {
-        case 0: return dispatch_step_ga<0>(a, f, sa, o, mom, nest, stream);
-        case 1: return dispatch_step_ga<1>(a, f, sa, o, mom, nest, stream);
-        case 2: return dispatch_step_ga<2>(a, f, sa, o, mom, nest, stream);
-        case 4: return dispatch_step_ga<4>(a, f, sa, o, mom, nest, stream);
-        case 8: return dispatch_step_ga<8>(a, f, sa, o, mom, nest, stream);
+        case 0: return dispatch_step_ga<0>(a, f, sa, o, mom, nest, mb, stream);
+        case 1: return dispatch_step_ga<1>(a, f, sa, o, mom, nest, mb, stream);
+        case 2: return dispatch_step_ga<2>(a, f, sa, o, mom, nest, mb, stream);
+        case 4: return dispatch_step_ga<4>(a, f, sa, o, mom, nest, mb, stream);
+        case 8: return dispatch_step_ga<8>(a, f, sa, o, mom, nest, mb, stream);
         default:
             return fail(SS_ERR_CONFIG, "gradient aggregation: world %d needs multicast (P2P widths 1, 2, 4, 8)", sa.world);
+    }
+}
+
+namespace {
+template <int W>
+int step_capacity(bool mom, bool nest, bool ga) {
+    int res;
+    if (ga) {
+        res = !mom ? occupancy(step_ga_kernel<false, false, W>, kThreads)
+                   : nest ? occupancy(step_ga_kernel<true, true, W>, kThreads)
+                          : occupancy(step_ga_kernel<true, false, W>, kThreads);
+    } else {
+        res = !mom ? occupancy(step_kernel<false, false, W>, kThreads)
+                   : nest ? occupancy(step_kernel<true, true, W>, kThreads)
+                          : occupancy(step_kernel<true, false, W>, kThreads);
+    }
+    int cap = ss_internal::sm_count() * res;
+    return cap < kMaxGrid ? cap : kMaxGrid;
+}
+}  // namespace
+
+extern "C" int ss_step_symm_grid_limit(const ss_symm_group* grp, int32_t momentum, int32_t nesterov, int32_t grads,
+                                       int32_t* blocks_out) {
+    if (!grp || !blocks_out) return fail(SS_ERR_CONFIG, "null argument");
+    if (grp->world < 1 || grp->world > kMaxRanks)
+        return fail(SS_ERR_CONFIG, "world size must be in [1, %d], got %d", kMaxRanks, grp->world);
+    const int w = grp->mc ? 0 : grp->world;
+    const bool mom = momentum != 0, nest = nesterov != 0, ga = grads != 0;
+    switch (w) {
+        case 0: *blocks_out = step_capacity<0>(mom, nest, ga); return SS_OK;
+        case 1: *blocks_out = step_capacity<1>(mom, nest, ga); return SS_OK;
+        case 2: *blocks_out = step_capacity<2>(mom, nest, ga); return SS_OK;
+        case 4: *blocks_out = step_capacity<4>(mom, nest, ga); return SS_OK;
+        case 8: *blocks_out = step_capacity<8>(mom, nest, ga); return SS_OK;
+        default:
+            return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 1, 2, 4, 8)", grp->world);
     }
 }

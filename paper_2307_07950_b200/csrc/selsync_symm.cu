@@ -40,7 +40,7 @@ namespace {
 
 constexpr int kThreads = 512;
 
-template <int W, int UO = 0, int LS = 0>
+template <int W>
 __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     __shared__ int s_word;
     __shared__ bool s_timeout;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     const int w = s_word;
     const bool sync = !s_timeout && w == SS_FLAG_SYNC;
     if (sync) {
-        average_shard<W, UO, LS>(a);
+        average_shard<W>(a);
         __threadfence_system();
     }
     __syncthreads();
@@ -93,62 +93,22 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     }
 }
 
-template <int W, int UO = 0, int LS = 0>
-int launch_symm_u(const SymmArgs& a, cudaStream_t s) {
+template <int W>
+int launch_symm(const SymmArgs& a, cudaStream_t s) {
     static int resident = 0;
     if (resident == 0) {
         int x = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, symm_sync_kernel<W, UO, LS>, kThreads, 0) != cudaSuccess || x <= 0) x = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x, symm_sync_kernel<W>, kThreads, 0) != cudaSuccess || x <= 0) x = 1;
         resident = x;
     }
     // all blocks co-resident: they never wait on each other, but the last
     // block's end barrier must not be starved behind queued blocks
     int grid = ss_internal::sm_count() * resident;
-    static int override_grid = -1;
-    if (override_grid < 0) {
-        const char* e = getenv("SS_SYMM_GRID");
-        override_grid = e ? atoi(e) : 0;
-    }
-    if (override_grid > 0 && override_grid < grid) grid = override_grid;
     const int64_t per_rank_vec = ((a.n >> 2) + a.world - 1) / a.world;
     const int64_t want = (per_rank_vec + kThreads * 4 - 1) / (kThreads * 4);
     if (want < grid) grid = static_cast<int>(want < 1 ? 1 : want);
-    symm_sync_kernel<W, UO, LS><<<grid, kThreads, 0, s>>>(a);
+    symm_sync_kernel<W><<<grid, kThreads, 0, s>>>(a);
     return ss_internal::check_launch("ss_symm_sync_f32");
-}
-
-// SS_SYMM_UNROLL overrides the vectors-in-flight per thread of the mean
-// (tuning sweeps, tools/symm_perf.py); widths 0 (NVLS), 2, 4, 8 only
-template <int W>
-int launch_symm(const SymmArgs& a, cudaStream_t s) {
-    static int u = -1;
-    if (u < 0) {
-        const char* e = getenv("SS_SYMM_UNROLL");
-        u = e ? atoi(e) : 0;
-    }
-    static int ls = -1;
-    if (ls < 0) {
-        const char* e = getenv("SS_P2P_VARIANT");
-        ls = e ? atoi(e) : 0;
-    }
-    if constexpr (W == 2) {
-        switch (ls) {
-            case 1: return launch_symm_u<W, 0, 1>(a, s);
-            case 2: return launch_symm_u<W, 0, 2>(a, s);
-            case 3: return launch_symm_u<W, 0, 3>(a, s);
-            default: break;
-        }
-    }
-    if constexpr (W == 0 || W == 2 || W == 4 || W == 8) {
-        switch (u) {
-            case 1: return launch_symm_u<W, 1>(a, s);
-            case 2: return launch_symm_u<W, 2>(a, s);
-            case 4: return launch_symm_u<W, 4>(a, s);
-            case 8: return launch_symm_u<W, 8>(a, s);
-            default: break;
-        }
-    }
-    return launch_symm_u<W, 0>(a, s);
 }
 
 }  // namespace
@@ -162,7 +122,7 @@ int ss_symm_group_layout(int64_t* offsets, int32_t cap, int32_t* count) {
         (int64_t)offsetof(ss_symm_group, agreed_ring), (int64_t)offsetof(ss_symm_group, err),
         (int64_t)offsetof(ss_symm_group, timeout_s),   (int64_t)offsetof(ss_symm_group, rank),
         (int64_t)offsetof(ss_symm_group, world),       (int64_t)offsetof(ss_symm_group, ring_cap),
-        (int64_t)offsetof(ss_symm_group, reserved),    (int64_t)offsetof(ss_symm_group, order_mode),
+        (int64_t)offsetof(ss_symm_group, max_blocks),    (int64_t)offsetof(ss_symm_group, order_mode),
         (int64_t)offsetof(ss_symm_group, order_threshold), (int64_t)offsetof(ss_symm_group, tile_cnt),
         (int64_t)offsetof(ss_symm_group, epoch),       (int64_t)offsetof(ss_symm_group, predictor),
         (int64_t)offsetof(ss_symm_group, tile_elems),  (int64_t)offsetof(ss_symm_group, n_tiles),
@@ -179,7 +139,7 @@ int ss_symm_group_layout(int64_t* offsets, int32_t cap, int32_t* count) {
 int ss_symm_signal_bytes(int32_t world, int64_t* bytes) {
     if (!bytes) return fail(SS_ERR_CONFIG, "null output");
     if (world < 1 || world > kMaxRanks) return fail(SS_ERR_CONFIG, "world size must be in [1, %d], got %d", kMaxRanks, world);
-    *bytes = 3 * static_cast<int64_t>(world) * static_cast<int64_t>(sizeof(uint64_t));
+    *bytes = 4 * static_cast<int64_t>(world) * static_cast<int64_t>(sizeof(uint64_t));
     return SS_OK;
 }
 

@@ -124,6 +124,11 @@ __device__ __forceinline__ uint64_t* vote_slot(const SymmArgs& a, int owner, uin
 __device__ __forceinline__ uint64_t* done_slot(const SymmArgs& a, int owner, int from) {
     return a.pads[owner] + 2 * a.world + from;
 }
+// poison tags (seq of the step): rank `from` met a NaN gradient in an update
+// tile of the known-sync pass, whose mean runs before the vote is in
+__device__ __forceinline__ uint64_t* poison_slot(const SymmArgs& a, int owner, int from) {
+    return a.pads[owner] + 3 * a.world + from;
+}
 
 // peer load / store flavours of the P2P mean (tuning: SS_P2P_VARIANT)
 template <int LS>

@@ -17,11 +17,14 @@ Device work per step, parameter aggregation (the default):
 
 Back ends (N > 1):
   collective="symm" (default): parameters live in symmetric memory.
-      flag_exchange="fused" (default): the whole step is ONE host launch
+      flag_exchange="fused" (default): the whole step is ONE cooperative launch
       (``ss_step_symm_f32``): update + norm + vote, the vote exchange over
-      NVLink in the last block, and on sync a device-side launch of the mean
-      (NVLS multimem or P2P, 1/N in the epilogue); ``order`` picks update-first,
-      norm-first (update and mean overlapped tile by tile) or adaptive.
+      NVLink in the last block to finish, which broadcasts the agreed word to
+      the rest of the grid; on sync every block then runs its part of the
+      mean (NVLS multimem or P2P, 1/N in the epilogue) and the last one the
+      end barrier -- no second launch. ``order`` picks update-first,
+      norm-first (update and mean overlapped tile by tile), adaptive, or
+      nan_safe (norm-first with the updates waiting for the vote).
       flag_exchange="p2p" / "nccl": K13, then ``ss_symm_sync_f32`` reading the
       agreed word (its own P2P exchange, or an NCCL allreduce-MAX before it).
       No host round-trip in any of them: ``step_async`` enqueues a whole step
@@ -30,9 +33,23 @@ Back ends (N > 1):
       issues NCCL allreduce-AVG on sync steps. ``fuse=False`` selects the
       pre-scale order instead: K1+K2, C1, K3 whose epilogue multiplies by 1/N
       when the agreed word says sync (the host read overlaps K3), allreduce-SUM.
+  Ranks sharing one GPU (``colocated.ColocatedSelSync``) use the symm back end
+  over same-device buffers, each rank on its own stream.
 
-Gradient aggregation (aggregation="grads", :395-399) uses the NCCL back end:
+Gradient aggregation (aggregation="grads", :395-399): over symmetric memory
+the one-launch ``ss_step_symm_ga_f32`` (norm + vote, then per tile the
+owner's mean of the GRADIENT and the update with it); on the NCCL back end
 K1+K2, C1, then on sync allreduce-AVG of the gradients, then the update.
+
+NaN semantics (``nan_safe=True``): the reference raises in observe
+(signal.py:67-68) before sgd_step (strategies.py:286 vs :383), so a NaN step
+mutates nothing. The fused update + norm pass updates before it knows the
+norm; with nan_safe the step uses an order in which every update waits for
+the agreed word and skips on an error bit (K1+K2 -> C1 -> K3, or the
+one-launch "nan_safe" order). Without it, only the rank that met the NaN is
+affected: no mean ever carries a NaN to another rank (the vote, or in the
+known-sync pass a per-tile poison tag, stops it), and SignalError is raised
+on every rank.
 """
 
 from __future__ import annotations
@@ -44,7 +61,7 @@ from typing import Optional
 import torch
 
 from . import kernels as K
-from .collectives import RankGroup, SymmetricParams
+from .collectives import RankGroup
 from .config import SelSyncConfig
 from .errors import ConfigError
 
@@ -69,6 +86,8 @@ class SelSyncStep:
         order_threshold: float = 0.2,
         tile_elems: Optional[int] = None,
         multicast="auto",
+        nan_safe: bool = False,
+        max_blocks: int = 0,
     ):
         if not isinstance(config, SelSyncConfig):
             raise ConfigError("config must be a SelSyncConfig")
@@ -79,12 +98,17 @@ class SelSyncStep:
         self.config = config
         self.device = params.device
         self.grads = grads
-        self.comm = group if isinstance(group, RankGroup) else RankGroup(group)
+        # a RankGroup, a rank group of ranks sharing one device (colocated), or a
+        # torch.distributed process group (None = WORLD)
+        self.comm = group if isinstance(group, RankGroup) or hasattr(group, "make_symmetric") else RankGroup(group)
         self.world = self.comm.size
         self.worker_id = self.comm.rank
+        colocated = self.comm.backend == "colocated"
         if collective is None:
-            collective = "symm" if (self.world > 1 and config.aggregation == "params"
-                                    and self.comm.backend == "nccl") else "nccl"
+            collective = "symm" if colocated or (self.world > 1 and config.aggregation == "params"
+                                                 and self.comm.backend == "nccl") else "nccl"
+        if colocated and collective != "symm":
+            raise ConfigError("colocated ranks exchange through the symmetric-memory step (collective='symm')")
         if collective not in ("nccl", "symm"):
             raise ConfigError(f"collective must be 'nccl' or 'symm', got {collective!r}")
         if flag_exchange is None:
@@ -96,8 +120,22 @@ class SelSyncStep:
         # one rank: no exchange -- unless symmetric memory is asked for explicitly
         # (the one-launch kernel on a single GPU, e.g. to profile it under ncu)
         self.collective = collective if (self.world > 1 or collective == "symm"
-                                        and torch.distributed.is_initialized()) else "none"
+                                        and (colocated or torch.distributed.is_initialized())) else "none"
         self.flag_exchange = flag_exchange
+        # NaN-safe: a step on which any rank observes a NaN norm changes no
+        # rank's parameters (the reference raises in observe, signal.py:67-68,
+        # before sgd_step, strategies.py:286 vs :383). The fused update + norm
+        # pass cannot promise that, so it gives way to K1+K2 -> C1 -> K3 (the
+        # pre-scale order, K3 skipping on an error word) or, over symmetric
+        # memory, to the one-launch step's "nan_safe" order.
+        self.nan_safe = bool(nan_safe) or order == "nan_safe"
+        if self.nan_safe:
+            if self.collective == "symm":
+                if flag_exchange != "fused" and config.aggregation == "params":
+                    raise ConfigError("nan_safe over symmetric memory is the one-launch step (flag_exchange='fused')")
+                order = "nan_safe"
+            else:
+                fuse = False
         self.fuse = (bool(fuse) or self.collective == "symm") and config.aggregation == "params"
         if self.collective == "symm" and config.aggregation == "grads" and flag_exchange != "fused":
             raise ConfigError("gradient aggregation over symmetric memory is the one-launch step "
@@ -114,10 +152,11 @@ class SelSyncStep:
         self.ws = K.Workspace(self.device)
         self.symm = None
         if self.collective == "symm":
-            self.symm = SymmetricParams(params.numel(), self.device, self.comm,
-                                        ring_capacity=trace_capacity, timeout_s=timeout_s,
-                                        order=order, order_threshold=order_threshold,
-                                        tile_elems=tile_elems, use_multicast=multicast)
+            self.symm = self.comm.make_symmetric(params.numel(), self.device,
+                                                 ring_capacity=trace_capacity, timeout_s=timeout_s,
+                                                 order=order, order_threshold=order_threshold,
+                                                 tile_elems=tile_elems, use_multicast=multicast,
+                                                 max_blocks=max_blocks)
             if config.aggregation == "grads":
                 # the exchanged vector is the gradient: it lives in symmetric memory
                 self.symm.buf.copy_(grads)
