@@ -77,10 +77,11 @@ def parse():
                     help="fused: the whole step in one cooperative launch (symm only)")
     ap.add_argument("--tile", type=int, default=None,
                     help="elements per tile of the overlapped sync step (default: 4096 up to 2M params, else 16384)")
-    ap.add_argument("--order", default="adaptive", choices=["update_first", "norm_first", "adaptive"],
+    ap.add_argument("--order", default="adaptive", choices=["update_first", "norm_first", "adaptive", "nan_safe"],
                     help="one-launch step order (flag-exchange fused): norm_first overlaps update and mean")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-replay", action="store_true", help="skip the replayed golden decision patterns")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
     return ap.parse_args()
 
@@ -226,7 +227,7 @@ def reference_arm(args, rank, world):
         "dtype": "fp64",
         "data": "synthetic",
         "config": workload_config(args, world),
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "host_cpus", "kind", "sample")},
         "e2e": {"value": base["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -309,17 +310,19 @@ def main():
 
     captured = {}  # --graph: one CUDA graph per (step object, gradient buffer)
 
-    def run(step, n, host_ring=None, host_row=None):
+    def run(step, n, host_ring=None, host_row=None, schedule=None):
         """n steps. Device-resident inputs: step_async (no host round-trip) when
         the step branches on the device. host_ring: the public blocking API with
         an H2D copy of the step's gradient from pinned host memory and a D2H of
-        the step's decision row inside every step."""
+        the step's decision row inside every step. schedule: ring index per step
+        (a replayed decision pattern) instead of the period-4 ring."""
         for _ in range(n):
-            k = step.steps_done % 4
+            k = step.steps_done % 4 if schedule is None else schedule[step.steps_done % len(schedule)]
             if host_ring is not None:
                 g.copy_(host_ring[k], non_blocking=True)
                 step.step(args.lr)
-                host_row.copy_(step.signal.trace[:32], non_blocking=True)
+                r = (step.steps_done - 1) % step.signal.trace_capacity  # this step's trace row
+                host_row.copy_(step.signal.trace[32 * r:32 * r + 32], non_blocking=True)
                 torch.cuda.current_stream().synchronize()
             elif args.graph and step.async_capable and step.steps_done > 0:
                 graphs = captured.setdefault(id(step), {})
@@ -388,6 +391,14 @@ def main():
         st = make_step(delta)
         run(st, max(3, args.warmup))
         modes[name] = timed(st, args.steps)
+    # ---- non-periodic mixes: the reference's own golden decision traces replayed
+    #      (sync <=> the gradient scale switches between 1.0 and 1.5: Delta >= 0.55)
+    replays = {}
+    if not args.no_replay:
+        for case, sched in replay_schedules().items():
+            st = make_step(0.3)
+            run(st, max(3, args.warmup), schedule=sched)
+            replays[case] = (timed(st, args.steps, schedule=sched), sched)
     # ---- C2 alone (NVLink roofline of the mean): ss_symm_sync_f32 with the word forced to sync
     c2 = None
     if world > 1 and args.collective == "symm":
@@ -450,9 +461,12 @@ def main():
     achieved = bytes_per_launch / (k_mean * 1e-3) / 1e9
     kernel_name = ("ss_update_norm_signal_f32 (K13+K2: fused SGD-momentum-wd update + ||g||^2 + signal step)"
                    if not args.no_fuse else "ss_norm_signal_f32 (K1+K2)")
+    traffic_key = "sgd_kernel" if not args.no_fuse else "norm_kernel"
     if one_launch:
-        kernel_name = ("ss_step_symm_f32 (one host launch: K13+K2 + P2P vote exchange; the NVLink "
-                       "mean is a device-side launch on sync steps only; timed on local steps)")
+        kernel_name = ("ss_step_symm_f32 (one cooperative launch: K13+K2, the P2P vote exchange in the last "
+                       "block, and on sync steps the NVLink mean by every block of the same grid; timed on "
+                       "local steps)")
+        traffic_key = f"step_kernel_w{world}"
     sync_frac = sum(1 for d in res["decisions"] if d) / len(res["decisions"])
     line = {
         "metric": METRIC,
@@ -477,7 +491,7 @@ def main():
             "peak_source": hbm_src,
             "unit": "GB/s",
             "frac": achieved / hbm_peak,
-            "traffic": traffic_from_profiles(P),
+            "traffic": traffic_from_profiles(traffic_key, P),
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "kernel_ms_mean": k_mean,
             "kernel_ms_median": kms[len(kms) // 2],
@@ -497,6 +511,13 @@ def main():
             ent["note"] = ("delta = 0: every step is sync before ||g||^2 is known, so the one-launch step "
                            "takes the known-sync pass (no norm sweep, mean overlapped from the first tile)")
         line["modes"][name] = ent
+    for case, (m, sched) in replays.items():
+        line["modes"][f"replay_{case}"] = {
+            "steps_per_s": world * args.steps / (m["ms"] / 1e3), "ms_per_step": m["ms"] / args.steps,
+            "sync_frac": sum(1 for d in m["decisions"] if d) / max(1, len(m["decisions"])),
+            "pattern": (f"post-warmup agreed decisions of the reference's golden {case} trace "
+                        f"({len(sched)} steps, cycled): not periodic, unlike the headline mix"),
+        }
     line.update({"exchange": exchange_stats(res, P, world)} if world > 1 else {})
     if one_launch and c2 is not None:
         line["exchange"] = c2
@@ -504,7 +525,7 @@ def main():
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_run(1, P, 3, 1, args, args.cpu_seconds)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "host_cpus", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -623,6 +644,30 @@ def model_bench(args, dev, comm, rank, world, local, hbm_peak, hbm_src):
         dist.destroy_process_group()
 
 
+def replay_schedules():
+    """Gradient-ring schedules that reproduce the agreed decisions of the
+    reference's golden n4_mixed / n8_mixed runs (tests/golden, made by the
+    unmodified reference): with smoothing 1 and delta 0.3 a step syncs iff its
+    gradient scale differs from the previous step's (ring 0 = 1.0, ring 2 = 1.5)."""
+    import numpy as np
+
+    z = np.load(ROOT / "tests" / "golden" / "selsync_cases.npz")
+    meta = json.loads(bytes(z["meta_json"]).decode())
+    out = {}
+    for case in ("n4_mixed", "n8_mixed"):
+        dec = z[f"{case}/decision"][:, 0][int(meta[case]["warmup"]):]
+        sched, cur = [], 0
+        for d in dec:
+            if d:
+                cur = 2 - cur
+            sched.append(cur)
+        if sched[0] == sched[-1]:  # the cycle's wrap-around must be local: same buffer
+            out[case] = sched
+        else:
+            out[case] = sched + sched  # even number of switches over the doubled cycle
+    return out
+
+
 def exchange_stats(m, P, world):
     """C1+C2 timing per step kind. Symmetric path: one event pair per step
     (local steps = flag agreement + early exit); NCCL path: pairs on sync
@@ -650,15 +695,15 @@ def exchange_stats(m, P, world):
     return out
 
 
-def traffic_from_profiles(P):
-    """dram read+write bytes per launch of the roofline kernel from the
-    committed ncu --set full summary for the same P, if one exists."""
+def traffic_from_profiles(kernel, P):
+    """dram read+write bytes per launch of THIS roofline kernel (sgd_kernel =
+    K13, step_kernel_w<N> = the one-launch step at N ranks, local step) from
+    the committed ncu --set full summaries at the same P, if one exists."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
     try:
-        d = json.loads(p.read_text())
-        ent = d.get(str(P))
+        ent = json.loads(p.read_text()).get(kernel, {}).get(str(P))
         return None if ent is None else ent["dram_bytes_per_launch"]
     except Exception:
         return None
