@@ -345,6 +345,7 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
     float* mb = MOM ? a.m + a.head : nullptr;
     const int64_t nvec = (a.n - a.head) >> 2;
     int64_t i = tid;
+#ifndef SS_K13_INDEX_LOOP  // A/B build switch (tools/ab_build.sh)
     if constexpr (U == 1) {
         // pointer-bumped loop with a 32-bit trip count: fewer live 64-bit
         // values than index arithmetic (keeps the 3-stream momentum pass in
@@ -371,6 +372,7 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
             }
         }
     } else
+#endif
     for (; i + (U - 1) * stride < nvec; i += U * stride) {
         float4 gv[U], wv[U], mv[U];
 #pragma unroll
@@ -393,7 +395,10 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
             if (MOM) st_pol<CP>(mb + k, mm);
         }
     }
-    if constexpr (U > 1) {  // with U == 1 the loop above covers every vector
+#ifndef SS_K13_INDEX_LOOP
+    if constexpr (U > 1)  // with U == 1 the loop above covers every vector
+#endif
+    {
         for (; i < nvec; i += stride) {
             const int64_t k = 4 * i;
             float4 gv = ld_cs4(gb + k), wv = ld_cs4(wb + k);

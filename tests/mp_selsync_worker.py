@@ -31,7 +31,8 @@ def main():
             "symm-p2p": dict(collective="symm", flag_exchange="p2p"),
             "symm-fused": dict(collective="symm", flag_exchange="fused"),
             "symm-normfirst": dict(collective="symm", flag_exchange="fused", order="norm_first"),
-            "symm-adaptive": dict(collective="symm", flag_exchange="fused", order="adaptive")}[mode]
+            "symm-adaptive": dict(collective="symm", flag_exchange="fused", order="adaptive"),
+            "symm-nansafe": dict(collective="symm", flag_exchange="fused", order="nan_safe")}[mode]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -102,7 +103,9 @@ def large_main():
             "two-launch": dict(collective="symm", flag_exchange="p2p"),
             "ga": dict(collective="symm", flag_exchange="fused"),
             "ga-nccl": dict(collective="nccl", fuse=True),
-            "bsp": dict(collective="symm", flag_exchange="fused", order="adaptive")}[variant]
+            "bsp": dict(collective="symm", flag_exchange="fused", order="adaptive"),
+            "nan_safe": dict(collective="symm", flag_exchange="fused", order="nan_safe"),
+            "nccl-nansafe": dict(collective="nccl", nan_safe=True)}[variant]
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -137,10 +140,21 @@ elif __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "nan")
     main()
 
 
+NAN_MODES = {"symm-adaptive": dict(collective="symm", order="adaptive"),
+             "symm-known": dict(collective="symm", order="adaptive"),  # warmup 8: the known-sync pass
+             "symm-update-first": dict(collective="symm", order="update_first"),
+             "symm-nansafe": dict(collective="symm", order="nan_safe"),
+             "nccl": dict(collective="nccl"),
+             "nccl-nansafe": dict(collective="nccl", nan_safe=True)}
+
+
 def nan_main():
     """A NaN gradient on ONE rank must raise SignalError on EVERY rank (the
-    error bit travels with the agreed word), and no rank may average."""
-    out = Path(sys.argv[2])
+    error bit travels with the agreed word), must never reach another rank's
+    parameters, and in the NaN-safe orders must leave every rank's
+    parameters and momentum untouched (signal.py:67-68 raises before
+    sgd_step, strategies.py:286 vs :383)."""
+    mode, out = sys.argv[2], Path(sys.argv[3])
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -148,20 +162,34 @@ def nan_main():
     dist.init_process_group("nccl", device_id=dev)
     from paper_2307_07950_b200 import SignalError
 
-    P = 4096
-    w = torch.zeros(P, device=dev)
-    g = torch.ones(P, device=dev)
-    step = SelSyncStep(w, g, SelSyncConfig(delta=0.1, warmup=1))
-    step.step_async(0.1)
+    P = 40_000
+    w = torch.from_numpy(np.random.default_rng(0).uniform(-0.05, 0.05, P).astype(np.float32)).to(dev)
+    g = torch.zeros(P, device=dev)
+    warmup = 8 if mode == "symm-known" else 1
+    cfg = SelSyncConfig(delta=0.1, warmup=warmup, smoothing=0.5, momentum=0.9, weight_decay=4e-4)
+    step = SelSyncStep(w, g, cfg, tile_elems=4096, **NAN_MODES[mode])
+    g = step.grads
+    for s in range(3):
+        g.copy_(torch.from_numpy(O.synthetic_grad32(5, rank, s, P)))
+        step.step(0.1)
+    before = step.params.clone()
+    mom = step.momentum.clone()
+    g.copy_(torch.from_numpy(O.synthetic_grad32(5, rank, 3, P)))
     if rank == 1:
-        g[7] = float("nan")
-    step.step_async(0.1)
+        g[P // 2 + 7] = float("nan")
     raised = False
     try:
-        step.synchronize()
+        if step.async_capable:
+            step.step_async(0.1)
+            step.synchronize()
+        else:
+            step.step(0.1)
     except SignalError:
         raised = True
-    np.savez(out / f"nan_rank{rank}.npz", raised=np.array(raised))
+    torch.cuda.synchronize()
+    np.savez(out / f"nan_{mode}_rank{rank}.npz", raised=np.array(raised),
+             finite=np.array(bool(torch.isfinite(step.params).all())),
+             unchanged=np.array(bool(torch.equal(step.params, before) and torch.equal(step.momentum, mom))))
     dist.barrier()
     dist.destroy_process_group()
 

@@ -32,7 +32,7 @@ def run_torchrun(n, name, mode, out):
 @pytest.mark.parametrize("name,n", [("n2_lam0.5", 2), ("cfg0_n2_d0.3", 2), ("n2_grads", 2), ("n4_mixed", 4),
                                     ("n4_grads", 4), ("n8_mixed", 8)])
 @pytest.mark.parametrize("mode", ["fused", "prescale", "symm-nccl", "symm-p2p", "symm-fused",
-                                  "symm-normfirst", "symm-adaptive"])
+                                  "symm-normfirst", "symm-adaptive", "symm-nansafe"])
 def test_nccl_ranks_match_reference(name, n, mode, tmp_path, golden_cases):
     if NGPU < n:
         pytest.skip(f"needs {n} GPUs")
@@ -47,14 +47,23 @@ def test_nccl_ranks_match_reference(name, n, mode, tmp_path, golden_cases):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-def test_nan_on_one_rank_raises_everywhere(tmp_path):
+@pytest.mark.parametrize("mode", ["symm-adaptive", "symm-known", "symm-update-first", "symm-nansafe", "nccl",
+                                  "nccl-nansafe"])
+def test_nan_on_one_rank_raises_everywhere(mode, tmp_path):
+    """SignalError on every rank; the NaN never reaches a healthy rank; in the
+    NaN-safe orders no rank's parameters or momentum change."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", "--master-port=29534",
-           str(ROOT / "tests" / "mp_selsync_worker.py"), "nan", str(tmp_path)]
+           str(ROOT / "tests" / "mp_selsync_worker.py"), "nan", mode, str(tmp_path)]
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     for r in range(2):
-        assert bool(np.load(tmp_path / f"nan_rank{r}.npz")["raised"])
+        z = np.load(tmp_path / f"nan_{mode}_rank{r}.npz")
+        assert bool(z["raised"])
+        if r != 1:
+            assert bool(z["finite"]), f"the NaN reached rank {r}"
+        if mode.endswith("nansafe"):
+            assert bool(z["unchanged"]), f"rank {r} changed on a NaN step"
 
 
 @pytest.fixture(scope="module")
@@ -81,7 +90,7 @@ def large_oracle():
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("n", [2, 4])
 @pytest.mark.parametrize("variant", ["nccl", "update_first", "norm_first", "adaptive", "p2p-mean", "nvls-mean",
-                                     "two-launch", "ga", "ga-nccl", "bsp"])
+                                     "two-launch", "ga", "ga-nccl", "bsp", "nan_safe", "nccl-nansafe"])
 def test_large_ragged_many_tiles_match_oracle(n, variant, tmp_path, large_oracle):
     """P = 1,000,003 in 4096-element tiles, momentum + weight decay, mixed
     decisions: the tile tickets, lag groups, scalar tail and every back end
