@@ -95,3 +95,32 @@ def test_graph_replay_matches_eager():
         torch.testing.assert_close(eager.flat.params, graphed.flat.params, rtol=1e-4, atol=1e-5)
     finally:
         torch.backends.cudnn.deterministic = False
+
+
+def test_trainer_metrics_rows_fill_loss_and_duration(tmp_path):
+    """SelSyncTrainer's metrics rows carry the loss and the step's device
+    time like the reference's MetricsRecord (strategies.py:326-339,
+    metrics.py:23-48), eager and graph-replayed iterations alike."""
+    from paper_2307_07950_b200 import trace as T
+
+    wl = W.build("resnet101", DEV, seed=5)
+    tr = SelSyncTrainer(wl, delta=0.05, warmup=2, smoothing=0.5)
+    x, y = wl.make_batch(0)
+    losses = [float(tr.train_step((x, y), wait=True)[0]) for _ in range(3)]
+    tr.capture((x.clone(), y.clone()), warmup_iters=2)
+    losses += [float("nan")] * 2  # the capture warm-up iterations ran on a side stream
+    for _ in range(3):
+        losses.append(float(tr.replay_step()))
+    rows = tr.metrics_rows()
+    assert [r["step"] for r in rows] == list(range(8))
+    for i, r in enumerate(rows):
+        assert set(r) == set(T.FIELDS)
+        assert r["step_duration"] > 0.0
+        assert r["lr"] == pytest.approx(wl.lr(i))
+        if not math.isnan(losses[i]):
+            assert r["loss"] == pytest.approx(losses[i], rel=1e-6)
+        assert math.isfinite(r["loss"])
+    out = tmp_path / "metrics.jsonl"
+    T.write_metrics_jsonl(rows, out)
+    back = T.load_metrics_jsonl(out)
+    assert [b["loss"] for b in back] == pytest.approx([r["loss"] for r in rows])
