@@ -302,12 +302,53 @@ SS_API int ss_step_symm_ga_f32(float* w_dev, float* g_dev, float* m_dev, int64_t
                                int32_t* word_dev, ss_trace_row* trace_dev, int32_t trace_cap,
                                const ss_symm_group* g_host, void* ws_dev, void* stream);
 
-/* Co-resident block capacity of this device for the one-launch step kernel
-   that ss_step_symm_f32 (grads = 0) or ss_step_symm_ga_f32 (grads = 1) would
-   launch for this group and these hyperparameters (#SMs x resident blocks).
-   Ranks sharing one device set max_blocks <= this / ranks. */
-SS_API int ss_step_symm_grid_limit(const ss_symm_group* g_host, int32_t momentum, int32_t nesterov,
-                                   int32_t grads, int32_t* blocks_out_host);
+/* ---------------- ranks sharing one device (colocated) ---------------- */
+
+/* One rank's arguments of ss_step_symm_f32 / ss_step_symm_ga_f32 except the
+   per-step lr and first-step flag. group is a HOST pointer read by prepare. */
+typedef struct ss_rank_step {
+    float* w_dev;
+    float* g_dev;
+    float* m_dev;
+    int64_t n;
+    float momentum;
+    float dampening;
+    float weight_decay;
+    int32_t nesterov;
+    ss_signal_state* st_dev;
+    double delta;
+    int32_t* word_dev;
+    ss_trace_row* trace_dev;
+    int32_t trace_cap;
+    int32_t reserved;
+    const ss_symm_group* group;
+    void* ws_dev;
+} ss_rank_step;
+
+typedef struct ss_colocated_plan {
+    void* args_dev;           /* in: caller-owned device buffer of ss_colocated_args_bytes(ranks) bytes */
+    int32_t ranks;            /* out */
+    int32_t blocks_per_rank;  /* out: G, each rank's slice of the launch */
+    int32_t grads;            /* out: 1 = gradient aggregation (ss_step_symm_ga_f32's kernel) */
+    int32_t flags;            /* out: bit 0 momentum, bit 1 Nesterov */
+} ss_colocated_plan;
+
+/* N ranks on ONE device (N = 1, 2, 4, 8; every rank's ss_symm_group holds the
+   other ranks' same-device buffers as its peers, mc = NULL) step together in
+   ONE cooperative launch of N x G blocks: blocks [r*G, (r+1)*G) run rank r's
+   one-launch step (the kernels of ss_step_symm_f32 / _ga_f32, bit-identical
+   work per rank) -- never as N launches that wait on one another, which
+   nothing guarantees to run at the same time. This is the reference's
+   N-worker round (runtime.py:275-294, :319-333) on a single GPU.
+   prepare validates every rank (as ss_step_symm_f32 does), picks G (the
+   rank's one-wave grid, capped so all N grids are co-resident; optionally
+   by max_blocks_per_rank) and copies the argument blocks into
+   plan->args_dev (synchronous on `stream`); step launches one step of all
+   ranks (CUDA-graph capturable). */
+SS_API int ss_colocated_args_bytes(int32_t ranks, int64_t* bytes_host);
+SS_API int ss_colocated_prepare_f32(const ss_rank_step* ranks_host, int32_t ranks, int32_t grads,
+                                    int32_t max_blocks_per_rank, ss_colocated_plan* plan_host, void* stream);
+SS_API int ss_colocated_step_f32(const ss_colocated_plan* plan_host, float lr, int32_t first_step, void* stream);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,24 @@ class SymmGroupC(Structure):
     ]
 
 
+class RankStepC(Structure):
+    """ss_rank_step -- one colocated rank's step arguments (pointers + hyperparameters)."""
+
+    _fields_ = [
+        ("w", c_void_p), ("g", c_void_p), ("m", c_void_p), ("n", c_int64),
+        ("momentum", c_float), ("dampening", c_float), ("weight_decay", c_float), ("nesterov", c_int32),
+        ("st", c_void_p), ("delta", c_double), ("word", c_void_p), ("trace", c_void_p),
+        ("trace_cap", c_int32), ("reserved", c_int32), ("group", c_void_p), ("ws", c_void_p),
+    ]
+
+
+class ColocatedPlanC(Structure):
+    """ss_colocated_plan."""
+
+    _fields_ = [("args_dev", c_void_p), ("ranks", c_int32), ("blocks_per_rank", c_int32), ("grads", c_int32),
+                ("flags", c_int32)]
+
+
 _P = c_void_p
 _SIGS = {
     "ss_abi_version": ([], c_int),
@@ -147,7 +165,9 @@ _SIGS = {
          _P, c_double, _P, _P, c_int32, POINTER(SymmGroupC), _P, _P],
         c_int,
     ),
-    "ss_step_symm_grid_limit": ([POINTER(SymmGroupC), c_int32, c_int32, c_int32, POINTER(c_int32)], c_int),
+    "ss_colocated_args_bytes": ([c_int32, POINTER(c_int64)], c_int),
+    "ss_colocated_prepare_f32": ([c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p], c_int),
+    "ss_colocated_step_f32": ([c_void_p, c_float, c_int32, c_void_p], c_int),
     "ss_step_symm_f32": (
         [_P, _P, _P, c_int64, c_float, c_float, c_float, c_float, c_int32, c_int32,
          _P, c_double, _P, _P, c_int32, POINTER(SymmGroupC), _P, _P],

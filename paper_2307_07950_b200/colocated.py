@@ -7,16 +7,19 @@ writes its peers' buffers over NVLink. Here the N ranks are N
 signal slots, tile counters, step counter, predictor, agreed ring and
 workspace, and its "peers" are the other ranks' same-device allocations --
 exactly the ``ss_symm_group`` layout the kernels expect, with plain device
-addresses instead of peer mappings. Each rank launches on its own CUDA stream
-and the grids split the device (``max_blocks`` = co-resident capacity / N),
-so all N grids are resident at once and the vote exchange, the tile tickets,
-the mean and the end barrier run as they do across GPUs -- the W = 2 / 4 / 8
-P2P instantiations of the kernels, ranks ordered and synchronised only by the
-device-side protocol (seq-tagged votes, release/acquire counters).
+addresses instead of peer mappings.
+
+Ranks whose kernels wait on one another must not be separate launches on one
+GPU (nothing guarantees that they run at the same time), so the N ranks step
+together in ONE cooperative launch (``ss_colocated_step_f32``): blocks
+[r*G, (r+1)*G) run rank r's one-launch step over rank r's arguments -- the
+same device code, per rank, as the per-GPU launch -- and the vote exchange,
+the tile tickets, the mean and the end barrier run between the slices as they
+do between GPUs (seq-tagged votes, release/acquire counters).
 
 This is the reference's N-worker exchange (flag relay runtime.py:319-333,
 mean round runtime.py:275-294 -> strategies.py:159-168, bootstrap
-runtime.py:178-191) through the same kernels a multi-GPU run uses, which a
+runtime.py:178-191) through the kernels a multi-GPU run uses, which a
 single-GPU box can run and check against the reference's golden traces.
 (The NVLS multicast path needs a multicast object over several GPUs and is
 not reachable this way.)
@@ -40,14 +43,13 @@ class ColocatedWorld:
     (or gradient) buffers, the N signal regions and the N tile-counter arrays
     every rank's ``ss_symm_group`` points into."""
 
-    def __init__(self, world: int, device, *, max_blocks: Optional[int] = None):
+    def __init__(self, world: int, device):
         if world < 1 or world > N.SYMM_MAX_RANKS:
             raise ConfigError(f"world must be in [1, {N.SYMM_MAX_RANKS}], got {world}")
         self.world = int(world)
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise ConfigError("colocated ranks need a CUDA device (no CPU fallback)")
-        self.max_blocks = max_blocks
         self.numel: Optional[int] = None
         self.views: dict[int, "ColocatedSymmetric"] = {}
         self.bcast: dict = {}
@@ -147,29 +149,23 @@ class ColocatedSymmetric(SymmetricView):
                          tile_cnt=[world.cnt[r].data_ptr() for r in range(world.world)],
                          ring_capacity=ring_capacity, timeout_s=timeout_s, order=order,
                          order_threshold=order_threshold, tile_elems=int(tile_elems),
-                         max_blocks=max_blocks or (world.max_blocks or 0))
+                         max_blocks=max_blocks)
         world.views[rank] = self
-
-    def grid_limit(self, *, momentum: bool, nesterov: bool, grads: bool) -> int:
-        out = ctypes.c_int32(0)
-        N.check(N.LIB.ss_step_symm_grid_limit(self.group_ref, int(momentum), int(nesterov), int(grads),
-                                              ctypes.byref(out)))
-        return int(out.value)
 
 
 class ColocatedSelSync:
-    """N SelSync ranks on one GPU, each a :class:`SelSyncStep` over the
-    one-launch symmetric-memory step kernels, each on its own CUDA stream.
+    """N SelSync ranks on one GPU, each a :class:`SelSyncStep` (state, trace,
+    buffers), stepped together by ONE cooperative launch per step.
 
     API as :class:`ReplicaSelSync` (``set_grads`` / ``step`` / ``decisions`` /
-    ``trace`` / ``params``), but every step is the multi-rank kernel itself:
-    ``step(lr)`` enqueues the N launches and returns; ``synchronize()`` waits
-    and raises ``SignalError`` / ``TransportError`` as ``SelSyncStep`` does.
+    ``trace`` / ``params``): ``step(lr)`` enqueues the launch and returns;
+    ``synchronize()`` waits and raises ``SignalError`` / ``TransportError`` as
+    ``SelSyncStep`` does; ``capture(lr)`` records the launch as a CUDA graph.
     """
 
     def __init__(self, init_params: torch.Tensor, n_ranks: int, config: SelSyncConfig, *,
                  order: str = "adaptive", order_threshold: float = 0.2, tile_elems: Optional[int] = None,
-                 timeout_s: float = 10.0, max_blocks: Optional[int] = None, trace_capacity: int = 4096,
+                 timeout_s: float = 10.0, max_blocks: int = 0, trace_capacity: int = 4096,
                  nan_safe: bool = False):
         from .step import SelSyncStep
 
@@ -181,8 +177,7 @@ class ColocatedSelSync:
         self.n = int(n_ranks)
         self.device = p0.device
         self.config = config
-        self.world = ColocatedWorld(self.n, self.device, max_blocks=max_blocks)
-        self.streams = [torch.cuda.Stream(self.device) for _ in range(self.n)]
+        self.world = ColocatedWorld(self.n, self.device)
         self.ranks: list = []
         for r in range(self.n):
             # only rank 0 holds the init; the others start from garbage and must
@@ -193,16 +188,24 @@ class ColocatedSelSync:
                              tile_elems=tile_elems, timeout_s=timeout_s, trace_capacity=trace_capacity,
                              nan_safe=nan_safe)
             self.ranks.append(st)
-        if max_blocks is None:
-            cap = self.ranks[0].symm.grid_limit(momentum=config.momentum != 0.0, nesterov=config.nesterov,
-                                               grads=config.aggregation == "grads")
-            per = cap // self.n
-            if per < 1:
-                raise ConfigError(f"{self.n} colocated grids do not fit on this device ({cap} resident blocks)")
-            max_blocks = per
-        for st in self.ranks:
-            st.symm.group_c.max_blocks = int(max_blocks)
-        self.max_blocks = int(max_blocks)
+        grads = config.aggregation == "grads"
+        table = (N.RankStepC * self.n)()
+        for r, st in enumerate(self.ranks):
+            c = st.config
+            table[r] = N.RankStepC(
+                st.params.data_ptr(), st.grads.data_ptr(),
+                st.momentum.data_ptr() if st.momentum is not None else None, st.params.numel(),
+                float(c.momentum), float(c.dampening), float(c.weight_decay), int(bool(c.nesterov)),
+                st.signal.state.data_ptr(), float(c.delta), st.signal.word.data_ptr(), st.signal.trace.data_ptr(),
+                st.signal.trace_capacity, 0, ctypes.addressof(st.symm.group_c), st.ws.ptr)
+        nbytes = ctypes.c_int64(0)
+        N.check(N.LIB.ss_colocated_args_bytes(self.n, ctypes.byref(nbytes)))
+        self._args = torch.empty(nbytes.value, dtype=torch.uint8, device=self.device)
+        self.plan = N.ColocatedPlanC(self._args.data_ptr(), 0, 0, 0, 0)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        N.check(N.LIB.ss_colocated_prepare_f32(ctypes.addressof(table), self.n, int(grads), int(max_blocks),
+                                               ctypes.addressof(self.plan), stream))
+        self.blocks_per_rank = int(self.plan.blocks_per_rank)
         torch.cuda.synchronize(self.device)
 
     @property
@@ -214,27 +217,39 @@ class ColocatedSelSync:
         return [st.grads for st in self.ranks]
 
     def set_grads(self, grads: Sequence[torch.Tensor]) -> None:
-        """Copy each rank's gradient on that rank's stream (ordered after its
-        previous step, as a backward on the rank's own GPU would be)."""
-        cur = torch.cuda.current_stream(self.device)
-        for st, s, g in zip(self.ranks, self.streams, grads):
-            s.wait_stream(cur)  # g may still be in flight on the caller's stream
-            with torch.cuda.stream(s):
-                st.grads.copy_(g.reshape(-1), non_blocking=True)
-            g.record_stream(s)
+        for st, g in zip(self.ranks, grads):
+            st.grads.copy_(g.reshape(-1), non_blocking=True)
+
+    def _launch(self, lr: float, stream) -> None:
+        from . import kernels as K
+
+        N.check(N.LIB.ss_colocated_step_f32(ctypes.addressof(self.plan), lr, int(self.steps_done == 0),
+                                            stream.cuda_stream))
+        K._count()
 
     def step(self, lr: float) -> None:
-        """Enqueue one step on every rank (N launches, no host round-trip)."""
-        for st, s in zip(self.ranks, self.streams):
-            with torch.cuda.stream(s):
-                st.step_async(lr)
+        """Enqueue one step of every rank (one launch, no host round-trip)."""
+        lr = self.ranks[0]._check_lr(lr)
+        self._launch(lr, torch.cuda.current_stream(self.device))
+        for st in self.ranks:
+            st._log_step(lr)
+
+    def capture(self, lr: float) -> "CapturedColocatedStep":
+        """Record one step of all ranks (the launch, this lr) as a CUDA graph."""
+        if self.steps_done == 0:
+            raise ConfigError("run one eager step first (the first step initialises the momentum buffers)")
+        lr = self.ranks[0]._check_lr(lr)
+        torch.cuda.synchronize(self.device)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self._launch(lr, torch.cuda.current_stream(self.device))
+        torch.cuda.synchronize(self.device)
+        return CapturedColocatedStep(self, graph, lr)
 
     def synchronize(self) -> None:
-        for s in self.streams:
-            s.synchronize()
-        for st, s in zip(self.ranks, self.streams):
-            with torch.cuda.stream(s):
-                st.synchronize()
+        torch.cuda.current_stream(self.device).synchronize()
+        for st in self.ranks:
+            st.synchronize()
 
     @property
     def steps_done(self) -> int:
@@ -248,3 +263,16 @@ class ColocatedSelSync:
 
     def records(self) -> list:
         return [row for st in self.ranks for row in st.records()]
+
+
+class CapturedColocatedStep:
+    def __init__(self, col: ColocatedSelSync, graph, lr: float):
+        self.col, self.graph, self.lr = col, graph, lr
+
+    def replay(self) -> None:
+        from . import kernels as K
+
+        self.graph.replay()
+        for st in self.col.ranks:
+            st._log_step(self.lr)
+        K._count()

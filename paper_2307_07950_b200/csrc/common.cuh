@@ -16,3 +16,19 @@ int check_launch(const char* what);
 int sm_count();
 
 }  // namespace ss_internal
+
+namespace {
+
+// A block's index within its rank's grid and that grid's size. A launch for
+// one rank uses blockIdx.x / gridDim.x; the colocated launch (the grids of
+// several ranks sharing one device in ONE cooperative launch) hands each rank
+// a contiguous slice of blocks.
+struct VBlk {
+    int bid;
+    int n;
+};
+__device__ __forceinline__ VBlk hw_blk() {
+    return VBlk{static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x)};
+}
+
+}  // namespace

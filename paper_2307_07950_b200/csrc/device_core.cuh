@@ -245,12 +245,12 @@ struct Finish {
 };
 
 // Deterministic two-pass finish inside the same launch.
-__device__ void finish_norm(const Finish& f, double acc) {
+__device__ void finish_norm(const Finish& f, double acc, VBlk vb) {
     __shared__ bool s_last;
     Workspace ws = ws_view(f.ws);
     double bsum = block_sum(acc);
     if (threadIdx.x == 0) {
-        ws.partials[f.block_offset + blockIdx.x] = bsum;
+        ws.partials[f.block_offset + vb.bid] = bsum;
         __threadfence();
         unsigned int prev = atomicAdd(ws.counter, 1u);
         s_last = (prev == static_cast<unsigned int>(f.total_blocks - 1));
@@ -267,14 +267,15 @@ __device__ void finish_norm(const Finish& f, double acc) {
         if (f.st) signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
     }
 }
+__device__ __forceinline__ void finish_norm(const Finish& f, double acc) { finish_norm(f, acc, hw_blk()); }
 
 // ---------------------------------------------------------------- K1 pass
 
 // this thread's fp64 partial of ||g||^2 over a grid-stride sweep
 template <int U>
-__device__ __forceinline__ double norm_pass(const float* __restrict__ g, int64_t n, int64_t head) {
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+__device__ __forceinline__ double norm_pass(const float* __restrict__ g, int64_t n, int64_t head, VBlk vb) {
+    const int64_t tid = static_cast<int64_t>(vb.bid) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(vb.n) * blockDim.x;
     double acc = 0.0;
     for (int64_t i = tid; i < head; i += stride) acc = fma((double)g[i], (double)g[i], acc);
     const float* gb = g + head;
@@ -290,6 +291,10 @@ __device__ __forceinline__ double norm_pass(const float* __restrict__ g, int64_t
     for (; i < nvec; i += stride) acc = sq4(ld_cs4(gb + 4 * i), acc);
     for (int64_t j = head + 4 * nvec + tid; j < n; j += stride) acc = fma((double)g[j], (double)g[j], acc);
     return acc;
+}
+template <int U>
+__device__ __forceinline__ double norm_pass(const float* __restrict__ g, int64_t n, int64_t head) {
+    return norm_pass<U>(g, n, head, hw_blk());
 }
 
 // ---------------------------------------------------------------- K3 / K13
@@ -319,9 +324,12 @@ __device__ __forceinline__ void sgd_elem(float& w, float g, float& m, const SgdA
 // One streaming pass of the update over the whole buffer; returns this
 // thread's fp64 partial of ||g||^2 (0 when NORM is false).
 template <bool MOM, bool NEST, bool NORM, int U, int CP = 0>
-__device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+__device__ __forceinline__ double sgd_pass(const SgdArgs& a_in, VBlk vb) {
+    // a register copy: a_in may live in shared memory (colocated launch), and
+    // stores through the generic w / m pointers would otherwise force reloads
+    const SgdArgs a = a_in;
+    const int64_t tid = static_cast<int64_t>(vb.bid) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(vb.n) * blockDim.x;
     float s = 1.0f;
     if (a.sync_word != nullptr) {
         const int word = __ldg(a.sync_word);
@@ -422,13 +430,18 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
     }
     return acc;
 }
+template <bool MOM, bool NEST, bool NORM, int U, int CP = 0>
+__device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
+    return sgd_pass<MOM, NEST, NORM, U, CP>(a, hw_blk());
+}
 
 // The update over elements [e0, e1) by the threads of ONE block (tile work of
 // the overlapped sync step). Requires 16-byte-aligned streams (head == 0) and
 // e0 % 4 == 0; a scalar tail is handled when e1 is not a multiple of 4.
 // NORM: also return this thread's fp64 partial of ||g||^2 over the range.
 template <bool MOM, bool NEST, int U = 2, bool G_L2 = false, bool NORM = false>
-__device__ __forceinline__ double sgd_block_range(const SgdArgs& a, int64_t e0, int64_t e1) {
+__device__ __forceinline__ double sgd_block_range(const SgdArgs& a_in, int64_t e0, int64_t e1) {
+    const SgdArgs a = a_in;  // register copy (see sgd_pass)
     // G_L2: read g through L2 only (it was just rewritten by peers over NVLink)
     // U vectors per stream in flight per thread: in the overlapped step only
     // part of the grid updates at a time, so each block needs more bytes in

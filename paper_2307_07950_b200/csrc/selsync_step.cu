@@ -48,6 +48,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 using ss_internal::check_launch;
@@ -157,7 +158,7 @@ __device__ int agreed_vote(const SymmArgs& s, uint64_t seq) {
 // last tile of this rank reduces the partials in tile order (deterministic),
 // runs K2 and posts this rank's vote.
 __device__ void known_tile_done(const Finish& f, const SymmArgs& s, const OverlapArgs& o, uint64_t seq, int N,
-                                int64_t T) {
+                                int64_t T, VBlk vb) {
     __shared__ bool s_last_tile;
     Workspace ws = ws_view(f.ws);
     if (threadIdx.x == 0) {
@@ -174,7 +175,7 @@ __device__ void known_tile_done(const Finish& f, const SymmArgs& s, const Overla
         *ws.counter = 0u;
         // K2 advances step_count, which every block reads once at kernel start
         // to pick this launch's order: run it only after all of them have
-        wait_count_gpu(o.started, gridDim.x, s);
+        wait_count_gpu(o.started, static_cast<unsigned int>(vb.n), s);
         signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
         const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
         __threadfence_system();
@@ -210,7 +211,7 @@ __device__ int order_snapshot(const Finish& f, const OverlapArgs& o) {
 
 template <bool MOM, bool NEST, int W>
 __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
-                                     uint64_t seq, bool known, bool safe) {
+                                     uint64_t seq, bool known, bool safe, VBlk vb) {
     __shared__ unsigned long long s_ticket;
     __shared__ int s_vote;
     __shared__ bool s_last;
@@ -232,17 +233,17 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     //      vote. Nobody waits here: blocks go straight on to the update tickets.
     if (!known) {
         Workspace ws = ws_view(f.ws);
-        const double bsum = block_sum(norm_pass<4>(a.g, a.n, a.head));
+        const double bsum = block_sum(norm_pass<4>(a.g, a.n, a.head, vb));
         if (threadIdx.x == 0) {
-            ws.partials[blockIdx.x] = bsum;
+            ws.partials[vb.bid] = bsum;
             __threadfence();
-            s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
+            s_last = atomicAdd(ws.counter, 1u) == static_cast<unsigned int>(vb.n - 1);
         }
         __syncthreads();
         if (s_last) {
             __threadfence();
             double v = 0.0;
-            for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
+            for (int i = threadIdx.x; i < vb.n; i += blockDim.x) v += __ldcg(ws.partials + i);
             v = block_sum(v);
             if (threadIdx.x == 0) {
                 *ws.counter = 0u;
@@ -306,7 +307,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                     // release at sys scope: the block's stores (ordered by the
                     // barrier) are visible to the owner before the count
                     if (threadIdx.x == 0) red_add_release_sys(o.cnt[t % N] + t, 1u);
-                    if (known) known_tile_done(f, s, o, seq, N, T);
+                    if (known) known_tile_done(f, s, o, seq, N, T, vb);
                     rec_tile = t;
                 }
             } else {
@@ -354,7 +355,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == static_cast<unsigned int>(vb.n - 1)) {
         const int w = (s_vote != -2 && !known) ? s_vote : agreed_vote(s, seq);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 4] = now_ns();
         *f.word = w;
@@ -378,27 +379,27 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
 // no second launch, no device-side launch.
 template <bool MOM, bool NEST, int W>
 __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
-                                     uint64_t seq) {
+                                     uint64_t seq, VBlk vb) {
     __shared__ bool s_last;
     __shared__ int s_w;
     uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;
     uint64_t* decided = reinterpret_cast<uint64_t*>(static_cast<char*>(f.ws) + 192);  // (seq << 32) | word
-    const double acc = sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a);
+    const double acc = sgd_pass<MOM, NEST, true, (MOM ? 1 : 2)>(a, vb);
     Workspace ws = ws_view(f.ws);
     const double bsum = block_sum(acc);
     if (threadIdx.x == 0) {
-        ws.partials[blockIdx.x] = bsum;
+        ws.partials[vb.bid] = bsum;
         // gpu scope suffices: the last block observes this counter and issues
         // the system-scope fence before its release of the vote (causality is
         // transitive), so peers reading after the vote see these stores
         __threadfence();
-        s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
+        s_last = atomicAdd(ws.counter, 1u) == static_cast<unsigned int>(vb.n - 1);
     }
     __syncthreads();
     if (s_last) {
         __threadfence();
         double v = 0.0;
-        for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
+        for (int i = threadIdx.x; i < vb.n; i += blockDim.x) v += __ldcg(ws.partials + i);
         v = block_sum(v);
         if (threadIdx.x == 0) {
             *ws.counter = 0u;
@@ -427,10 +428,10 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
         if (s_last && threadIdx.x == 0) *s.seq = static_cast<uint32_t>(seq);
         return;
     }
-    average_shard<W>(s);
+    average_shard<W>(s, vb);
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == static_cast<unsigned int>(vb.n - 1)) {
         end_barrier(s, seq);
         *s.arrive = 0u;
         *s.seq = static_cast<uint32_t>(seq);
@@ -438,17 +439,23 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
 }
 
 template <bool MOM, bool NEST, int W>
-__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
+__device__ __forceinline__ void step_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
+                                          VBlk vb) {
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     // the order of this step: identical on every rank (same decision history)
     const int order = order_snapshot(f, o);
     uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {start, vote posted, votes in, -, last arrival, end}
-    if (mark && blockIdx.x == 0 && threadIdx.x == 0) mark[0] = now_ns();
+    if (mark && vb.bid == 0 && threadIdx.x == 0) mark[0] = now_ns();
     if (order & kNormFirst) {
-        nf_body<MOM, NEST, W>(a, f, s, o, seq, (order & kKnown) != 0, (order & kSafe) != 0);
+        nf_body<MOM, NEST, W>(a, f, s, o, seq, (order & kKnown) != 0, (order & kSafe) != 0, vb);
         return;
     }
-    uf_body<MOM, NEST, W>(a, f, s, o, seq);
+    uf_body<MOM, NEST, W>(a, f, s, o, seq, vb);
+}
+
+template <bool MOM, bool NEST, int W>
+__global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
+    step_body<MOM, NEST, W>(a, f, s, o, hw_blk());
 }
 
 // ------------------------------------------- gradient aggregation, one launch
@@ -463,7 +470,8 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, 
 // sync step -- waits for its tile's announcement. On a local step no ticket
 // waits and the update uses the rank's own gradient.
 template <bool MOM, bool NEST, int W>
-__global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
+__device__ __forceinline__ void ga_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
+                                        VBlk vb) {
     __shared__ unsigned long long s_ticket;
     __shared__ int s_vote;
     __shared__ bool s_last;
@@ -476,17 +484,17 @@ __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish 
     if (threadIdx.x == 0) s_vote = -2;
     {   // ---- ||g||^2 sweep; the last block runs K2 and posts the vote
         Workspace ws = ws_view(f.ws);
-        const double bsum = block_sum(norm_pass<4>(a.g, a.n, a.head));
+        const double bsum = block_sum(norm_pass<4>(a.g, a.n, a.head, vb));
         if (threadIdx.x == 0) {
-            ws.partials[blockIdx.x] = bsum;
+            ws.partials[vb.bid] = bsum;
             __threadfence();
-            s_last = atomicAdd(ws.counter, 1u) == gridDim.x - 1;
+            s_last = atomicAdd(ws.counter, 1u) == static_cast<unsigned int>(vb.n - 1);
         }
         __syncthreads();
         if (s_last) {
             __threadfence();
             double v = 0.0;
-            for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) v += __ldcg(ws.partials + i);
+            for (int i = threadIdx.x; i < vb.n; i += blockDim.x) v += __ldcg(ws.partials + i);
             v = block_sum(v);
             if (threadIdx.x == 0) {
                 *ws.counter = 0u;
@@ -549,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish 
     }
     __threadfence_system();
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == gridDim.x - 1) {
+    if (threadIdx.x == 0 && atomicAdd(s.arrive, 1u) == static_cast<unsigned int>(vb.n - 1)) {
         *f.word = s_vote;
         if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = s_vote;
         if (sync) {
@@ -560,6 +568,11 @@ __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish 
         *s.arrive = 0u;
         *s.seq = static_cast<uint32_t>(seq);
     }
+}
+
+template <bool MOM, bool NEST, int W>
+__global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
+    ga_body<MOM, NEST, W>(a, f, s, o, hw_blk());
 }
 
 template <typename K>
@@ -655,10 +668,21 @@ int dispatch_step_ga(const SgdArgs& a, const Finish& f, const SymmArgs& sa, cons
 
 }  // namespace
 
-extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, float lr, float momentum,
-                                float dampening, float weight_decay, int32_t nesterov, int32_t first_step,
-                                ss_signal_state* st, double delta, int32_t* word, ss_trace_row* trace,
-                                int32_t cap, const ss_symm_group* grp, void* ws, void* stream) {
+namespace {
+
+// Argument blocks of one rank's one-launch step (both aggregation modes),
+// validated. The host-launch entry points and the colocated plan share it.
+struct RankArgs {
+    SgdArgs a;
+    Finish f;
+    SymmArgs s;
+    OverlapArgs o;
+};
+
+int build_rank_args(bool ga, float* w, float* g, float* m, int64_t n, float lr, float momentum, float dampening,
+                    float weight_decay, int32_t nesterov, int32_t first_step, ss_signal_state* st, double delta,
+                    int32_t* word, ss_trace_row* trace, int32_t cap, const ss_symm_group* grp, void* ws,
+                    RankArgs* out) {
     SgdArgs a;
     int rc = make_sgd_args(&a, w, g, m, n, lr, momentum, dampening, weight_decay, nesterov, first_step,
                            nullptr, 1.0f);
@@ -672,43 +696,133 @@ extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, f
     rc = symm_args_from_group(grp, n, word, 1, 1.0f / static_cast<float>(grp ? grp->world : 1), ws, &sa,
                               &ss_internal::fail);
     if (rc) return rc;
-    if (grp->bufs[grp->rank] != w) return fail(SS_ERR_CONFIG, "w must be this rank's symmetric buffer");
+    if (grp->max_blocks < 0) return fail(SS_ERR_CONFIG, "max_blocks must be >= 0, got %d", grp->max_blocks);
     OverlapArgs o{};
     o.dbg = grp->debug_events;
     o.dbg_cap = grp->debug_events ? grp->debug_cap : 0;
-    o.mode = grp->order_mode;
+    o.mode = ga ? 0 : grp->order_mode;
     o.threshold = grp->order_threshold;
     o.started = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 224);
-    if (o.mode < 0 || o.mode > 3) return fail(SS_ERR_CONFIG, "order_mode must be 0, 1, 2 or 3, got %d", o.mode);
-    if (o.mode != 0) {
-        if (a.head != 0) return fail(SS_ERR_CONFIG, "norm-first order needs 16-byte aligned w, g, m");
-        if (!grp->epoch || !grp->predictor || grp->tile_elems <= 0 || (grp->tile_elems & 3))
-            return fail(SS_ERR_CONFIG, "norm-first order needs epoch, predictor and a tile size (multiple of 4)");
+    o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
+    const bool tiled = ga || o.mode != 0;
+    if (ga) {
+        if (grp->bufs[grp->rank] != g) return fail(SS_ERR_CONFIG, "g must be this rank's symmetric buffer");
+        if (a.head != 0) return fail(SS_ERR_CONFIG, "gradient aggregation needs 16-byte aligned w, g, m");
+        if (!grp->epoch || grp->tile_elems <= 0 || (grp->tile_elems & 3))
+            return fail(SS_ERR_CONFIG, "gradient aggregation needs epoch and a tile size (multiple of 4)");
+    } else {
+        if (grp->bufs[grp->rank] != w) return fail(SS_ERR_CONFIG, "w must be this rank's symmetric buffer");
+        if (o.mode < 0 || o.mode > 3) return fail(SS_ERR_CONFIG, "order_mode must be 0, 1, 2 or 3, got %d", o.mode);
+        if (o.mode != 0) {
+            if (a.head != 0) return fail(SS_ERR_CONFIG, "norm-first order needs 16-byte aligned w, g, m");
+            if (!grp->epoch || !grp->predictor || grp->tile_elems <= 0 || (grp->tile_elems & 3))
+                return fail(SS_ERR_CONFIG, "norm-first order needs epoch, predictor and a tile size (multiple of 4)");
+        }
+    }
+    if (tiled) {
         const int64_t tiles = (n + grp->tile_elems - 1) / grp->tile_elems;
         if (tiles > grp->n_tiles) return fail(SS_ERR_CONFIG, "tile counters hold %lld tiles, need %lld",
                                              (long long)grp->n_tiles, (long long)tiles);
-        for (int r = 0; r < grp->world; ++r)
-            if (!grp->tile_cnt[r]) return fail(SS_ERR_CONFIG, "null tile counters for rank %d", r);
-        for (int r = 0; r < kMaxRanks; ++r) o.cnt[r] = r < grp->world ? grp->tile_cnt[r] : nullptr;
+        for (int r = 0; r < kMaxRanks; ++r) {
+            if (r < grp->world && !grp->tile_cnt[r]) return fail(SS_ERR_CONFIG, "null tile counters for rank %d", r);
+            o.cnt[r] = r < grp->world ? grp->tile_cnt[r] : nullptr;
+        }
         o.epoch = grp->epoch;
         o.predictor = grp->predictor;
         o.tile = grp->tile_elems;
         o.n_tiles = tiles;
-        o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
-        o.tile_norm = grp->tile_norm;
+        if (!ga) o.tile_norm = grp->tile_norm;
     }
-    if (grp->max_blocks < 0) return fail(SS_ERR_CONFIG, "max_blocks must be >= 0, got %d", grp->max_blocks);
-    const int mb = grp->max_blocks;
-    Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
+    out->a = a;
+    out->f = Finish{ws, 0, 0, nullptr, st, delta, word, trace, cap};
+    out->s = sa;
+    out->o = o;
+    return SS_OK;
+}
+
+// ------------------------------------------------ colocated ranks, one launch
+//
+// Ranks that share ONE device must not run as separate launches that wait on
+// one another (nothing guarantees that they run at the same time). Their
+// grids are therefore one cooperative launch: blocks [r*G, (r+1)*G) are rank
+// r's grid of G blocks, each running exactly the code of the per-rank launch
+// over its rank's argument block (kept in device memory, copied to shared
+// memory per block) with its slice index as the block index.
+
+__device__ __forceinline__ const RankArgs& load_rank_args(const RankArgs* __restrict__ args, int rank, float lr,
+                                                          int first) {
+    __shared__ __align__(16) RankArgs s_ra;
+    static_assert(sizeof(RankArgs) % 16 == 0, "RankArgs copies in 16-byte vectors");
+    const uint4* src = reinterpret_cast<const uint4*>(args + rank);
+    uint4* dst = reinterpret_cast<uint4*>(&s_ra);
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(RankArgs) / 16); i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_ra.a.lr = lr;
+        s_ra.a.first = first;
+    }
+    __syncthreads();
+    return s_ra;
+}
+
+template <bool MOM, bool NEST, int W>
+__global__ void __launch_bounds__(kThreads, 4) step_kernel_colo(const RankArgs* __restrict__ args, int per_rank,
+                                                                float lr, int first) {
+    const int rank = static_cast<int>(blockIdx.x) / per_rank;
+    const RankArgs& ra = load_rank_args(args, rank, lr, first);
+    step_body<MOM, NEST, W>(ra.a, ra.f, ra.s, ra.o, VBlk{static_cast<int>(blockIdx.x) % per_rank, per_rank});
+}
+
+template <bool MOM, bool NEST, int W>
+__global__ void __launch_bounds__(kThreads, 4) step_ga_kernel_colo(const RankArgs* __restrict__ args, int per_rank,
+                                                                   float lr, int first) {
+    const int rank = static_cast<int>(blockIdx.x) / per_rank;
+    const RankArgs& ra = load_rank_args(args, rank, lr, first);
+    ga_body<MOM, NEST, W>(ra.a, ra.f, ra.s, ra.o, VBlk{static_cast<int>(blockIdx.x) % per_rank, per_rank});
+}
+
+template <bool MOM, bool NEST, int W>
+void* colo_kernel(bool ga) {
+    return ga ? reinterpret_cast<void*>(step_ga_kernel_colo<MOM, NEST, W>)
+              : reinterpret_cast<void*>(step_kernel_colo<MOM, NEST, W>);
+}
+
+template <int W>
+void* colo_kernel_for(bool ga, bool mom, bool nest) {
+    if (!mom) return colo_kernel<false, false, W>(ga);
+    return nest ? colo_kernel<true, true, W>(ga) : colo_kernel<true, false, W>(ga);
+}
+
+void* colo_kernel_any(int ranks, bool ga, bool mom, bool nest) {
+    switch (ranks) {
+        case 1: return colo_kernel_for<1>(ga, mom, nest);
+        case 2: return colo_kernel_for<2>(ga, mom, nest);
+        case 4: return colo_kernel_for<4>(ga, mom, nest);
+        case 8: return colo_kernel_for<8>(ga, mom, nest);
+        default: return nullptr;
+    }
+}
+
+}  // namespace
+
+extern "C" int ss_step_symm_f32(float* w, const float* g, float* m, int64_t n, float lr, float momentum,
+                                float dampening, float weight_decay, int32_t nesterov, int32_t first_step,
+                                ss_signal_state* st, double delta, int32_t* word, ss_trace_row* trace,
+                                int32_t cap, const ss_symm_group* grp, void* ws, void* stream) {
+    RankArgs r;
+    const int rc = build_rank_args(false, w, const_cast<float*>(g), m, n, lr, momentum, dampening, weight_decay,
+                                   nesterov, first_step, st, delta, word, trace, cap, grp, ws, &r);
+    if (rc) return rc;
     const bool mom = momentum != 0.0f, nest = nesterov != 0;
-    switch (symm_width(sa)) {
-        case 0: return dispatch_step<0>(a, f, sa, o, mom, nest, mb, stream);
-        case 1: return dispatch_step<1>(a, f, sa, o, mom, nest, mb, stream);  // single rank (profiling)
-        case 2: return dispatch_step<2>(a, f, sa, o, mom, nest, mb, stream);
-        case 4: return dispatch_step<4>(a, f, sa, o, mom, nest, mb, stream);
-        case 8: return dispatch_step<8>(a, f, sa, o, mom, nest, mb, stream);
+    const int mb = grp->max_blocks;
+    switch (symm_width(r.s)) {
+        case 0: return dispatch_step<0>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
+        case 1: return dispatch_step<1>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);  // single rank (profiling)
+        case 2: return dispatch_step<2>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
+        case 4: return dispatch_step<4>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
+        case 8: return dispatch_step<8>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
         default:
-            return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 1, 2, 4, 8)", sa.world);
+            return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 1, 2, 4, 8)", r.s.world);
     }
 }
 
@@ -716,84 +830,109 @@ extern "C" int ss_step_symm_ga_f32(float* w, float* g, float* m, int64_t n, floa
                                    float dampening, float weight_decay, int32_t nesterov, int32_t first_step,
                                    ss_signal_state* st, double delta, int32_t* word, ss_trace_row* trace,
                                    int32_t cap, const ss_symm_group* grp, void* ws, void* stream) {
-    SgdArgs a;
-    int rc = make_sgd_args(&a, w, g, m, n, lr, momentum, dampening, weight_decay, nesterov, first_step,
-                           nullptr, 1.0f);
+    RankArgs r;
+    const int rc = build_rank_args(true, w, g, m, n, lr, momentum, dampening, weight_decay, nesterov, first_step,
+                                   st, delta, word, trace, cap, grp, ws, &r);
     if (rc) return rc;
-    if (!st || !ws || !word) return fail(SS_ERR_CONFIG, "null state/word/workspace");
-    rc = check_delta_impl(delta);
-    if (rc) return rc;
-    rc = check_trace(trace, cap);
-    if (rc) return rc;
-    SymmArgs sa;
-    rc = symm_args_from_group(grp, n, word, 1, 1.0f / static_cast<float>(grp ? grp->world : 1), ws, &sa,
-                              &ss_internal::fail);
-    if (rc) return rc;
-    if (grp->bufs[grp->rank] != g) return fail(SS_ERR_CONFIG, "g must be this rank's symmetric buffer");
-    if (a.head != 0) return fail(SS_ERR_CONFIG, "gradient aggregation needs 16-byte aligned w, g, m");
-    if (!grp->epoch || grp->tile_elems <= 0 || (grp->tile_elems & 3))
-        return fail(SS_ERR_CONFIG, "gradient aggregation needs epoch and a tile size (multiple of 4)");
-    OverlapArgs o{};
-    const int64_t tiles = (n + grp->tile_elems - 1) / grp->tile_elems;
-    if (tiles > grp->n_tiles) return fail(SS_ERR_CONFIG, "tile counters hold %lld tiles, need %lld",
-                                         (long long)grp->n_tiles, (long long)tiles);
-    for (int r = 0; r < kMaxRanks; ++r) {
-        if (r < grp->world && !grp->tile_cnt[r]) return fail(SS_ERR_CONFIG, "null tile counters for rank %d", r);
-        o.cnt[r] = r < grp->world ? grp->tile_cnt[r] : nullptr;
-    }
-    o.epoch = grp->epoch;
-    o.predictor = grp->predictor;
-    o.tile = grp->tile_elems;
-    o.n_tiles = tiles;
-    o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
-    o.started = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 224);
-    if (grp->max_blocks < 0) return fail(SS_ERR_CONFIG, "max_blocks must be >= 0, got %d", grp->max_blocks);
-    const int mb = grp->max_blocks;
-    Finish f{ws, 0, 0, nullptr, st, delta, word, trace, cap};
     const bool mom = momentum != 0.0f, nest = nesterov != 0;
-    switch (symm_width(sa)) {
-        case 0: return dispatch_step_ga<0>(a, f, sa, o, mom, nest, mb, stream);
-        case 1: return dispatch_step_ga<1>(a, f, sa, o, mom, nest, mb, stream);
-        case 2: return dispatch_step_ga<2>(a, f, sa, o, mom, nest, mb, stream);
-        case 4: return dispatch_step_ga<4>(a, f, sa, o, mom, nest, mb, stream);
-        case 8: return dispatch_step_ga<8>(a, f, sa, o, mom, nest, mb, stream);
+    const int mb = grp->max_blocks;
+    switch (symm_width(r.s)) {
+        case 0: return dispatch_step_ga<0>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
+        case 1: return dispatch_step_ga<1>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
+        case 2: return dispatch_step_ga<2>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
+        case 4: return dispatch_step_ga<4>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
+        case 8: return dispatch_step_ga<8>(r.a, r.f, r.s, r.o, mom, nest, mb, stream);
         default:
-            return fail(SS_ERR_CONFIG, "gradient aggregation: world %d needs multicast (P2P widths 1, 2, 4, 8)", sa.world);
+            return fail(SS_ERR_CONFIG, "gradient aggregation: world %d needs multicast (P2P widths 1, 2, 4, 8)",
+                        r.s.world);
     }
 }
 
-namespace {
-template <int W>
-int step_capacity(bool mom, bool nest, bool ga) {
-    int res;
-    if (ga) {
-        res = !mom ? occupancy(step_ga_kernel<false, false, W>, kThreads)
-                   : nest ? occupancy(step_ga_kernel<true, true, W>, kThreads)
-                          : occupancy(step_ga_kernel<true, false, W>, kThreads);
-    } else {
-        res = !mom ? occupancy(step_kernel<false, false, W>, kThreads)
-                   : nest ? occupancy(step_kernel<true, true, W>, kThreads)
-                          : occupancy(step_kernel<true, false, W>, kThreads);
-    }
-    int cap = ss_internal::sm_count() * res;
-    return cap < kMaxGrid ? cap : kMaxGrid;
+extern "C" int ss_colocated_args_bytes(int32_t ranks, int64_t* bytes) {
+    if (!bytes) return fail(SS_ERR_CONFIG, "null output");
+    if (ranks != 1 && ranks != 2 && ranks != 4 && ranks != 8)
+        return fail(SS_ERR_CONFIG, "colocated ranks: 1, 2, 4 or 8 (the P2P widths of the step kernel), got %d", ranks);
+    *bytes = static_cast<int64_t>(ranks) * static_cast<int64_t>(sizeof(RankArgs));
+    return SS_OK;
 }
-}  // namespace
 
-extern "C" int ss_step_symm_grid_limit(const ss_symm_group* grp, int32_t momentum, int32_t nesterov, int32_t grads,
-                                       int32_t* blocks_out) {
-    if (!grp || !blocks_out) return fail(SS_ERR_CONFIG, "null argument");
-    if (grp->world < 1 || grp->world > kMaxRanks)
-        return fail(SS_ERR_CONFIG, "world size must be in [1, %d], got %d", kMaxRanks, grp->world);
-    const int w = grp->mc ? 0 : grp->world;
-    const bool mom = momentum != 0, nest = nesterov != 0, ga = grads != 0;
-    switch (w) {
-        case 0: *blocks_out = step_capacity<0>(mom, nest, ga); return SS_OK;
-        case 1: *blocks_out = step_capacity<1>(mom, nest, ga); return SS_OK;
-        case 2: *blocks_out = step_capacity<2>(mom, nest, ga); return SS_OK;
-        case 4: *blocks_out = step_capacity<4>(mom, nest, ga); return SS_OK;
-        case 8: *blocks_out = step_capacity<8>(mom, nest, ga); return SS_OK;
-        default:
-            return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 1, 2, 4, 8)", grp->world);
+extern "C" int ss_colocated_prepare_f32(const ss_rank_step* rs, int32_t ranks, int32_t grads,
+                                        int32_t max_blocks_per_rank, ss_colocated_plan* plan, void* stream) {
+    int64_t bytes = 0;
+    int rc = ss_colocated_args_bytes(ranks, &bytes);
+    if (rc) return rc;
+    if (!rs || !plan || !plan->args_dev) return fail(SS_ERR_CONFIG, "null rank table / plan / plan->args_dev");
+    if (max_blocks_per_rank < 0) return fail(SS_ERR_CONFIG, "max_blocks_per_rank must be >= 0");
+    const bool ga = grads != 0;
+    const bool mom = rs[0].momentum != 0.0f, nest = rs[0].nesterov != 0;
+    RankArgs host[SS_SYMM_MAX_RANKS];
+    for (int r = 0; r < ranks; ++r) {
+        const ss_rank_step& x = rs[r];
+        if (!x.group) return fail(SS_ERR_CONFIG, "rank %d: null group", r);
+        if (x.group->world != ranks || x.group->rank != r)
+            return fail(SS_ERR_CONFIG, "rank %d: group says rank %d of %d", r, x.group->rank, x.group->world);
+        if (x.group->mc) return fail(SS_ERR_CONFIG, "colocated ranks have no multicast address");
+        if (x.n != rs[0].n || (x.momentum != 0.0f) != mom || (x.nesterov != 0) != nest)
+            return fail(SS_ERR_CONFIG, "rank %d: every colocated rank needs the same size and update kind", r);
+        rc = build_rank_args(ga, x.w_dev, x.g_dev, x.m_dev, x.n, 0.0f, x.momentum, x.dampening, x.weight_decay,
+                             x.nesterov, 0, x.st_dev, x.delta, x.word_dev, x.trace_dev, x.trace_cap, x.group, x.ws_dev,
+                             &host[r]);
+        if (rc) {
+            char msg[384];
+            snprintf(msg, sizeof(msg), "%s", ss_last_error());
+            return fail(rc, "rank %d: %s", r, msg);
+        }
     }
+    // one cooperative launch of ranks x G blocks: G = this rank's one-wave grid,
+    // capped so that all ranks' grids are co-resident together
+    void* kern = colo_kernel_any(ranks, ga, mom, nest);
+    int res = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res, kern, kThreads, 0) != cudaSuccess || res <= 0)
+        return check_launch("ss_colocated_prepare_f32 (occupancy)");
+    const int cap = ss_internal::sm_count() * res / ranks;
+    if (cap < 1) return fail(SS_ERR_CONFIG, "%d colocated grids do not fit on this device", ranks);
+    int per_rank = static_cast<int>(grid_for((host[0].a.n - host[0].a.head) / 4 + 1, mom ? 1 : 2, res));
+    if (per_rank > cap) per_rank = cap;
+    if (max_blocks_per_rank > 0 && per_rank > max_blocks_per_rank) per_rank = max_blocks_per_rank;
+    for (int r = 0; r < ranks; ++r) {
+        host[r].f.total_blocks = per_rank;
+        host[r].o.lag = per_rank / (ranks + 1) + 2;
+    }
+    if (cudaMemcpyAsync(plan->args_dev, host, static_cast<size_t>(bytes), cudaMemcpyHostToDevice,
+                        static_cast<cudaStream_t>(stream)) != cudaSuccess ||
+        cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess)
+        return check_launch("ss_colocated_prepare_f32 (argument copy)");
+    plan->ranks = ranks;
+    plan->blocks_per_rank = per_rank;
+    plan->grads = ga ? 1 : 0;
+    plan->flags = (mom ? 1 : 0) | (nest ? 2 : 0);
+    return SS_OK;
+}
+
+extern "C" int ss_colocated_step_f32(const ss_colocated_plan* plan, float lr, int32_t first_step, void* stream) {
+    if (!plan || !plan->args_dev || plan->blocks_per_rank < 1) return fail(SS_ERR_CONFIG, "plan not prepared");
+    if (!(lr >= 0.0f)) return fail(SS_ERR_CONFIG, "learning rate must be non-negative, got %g", (double)lr);
+    const bool ga = plan->grads != 0, mom = plan->flags & 1, nest = (plan->flags & 2) != 0;
+    void* kern = colo_kernel_any(plan->ranks, ga, mom, nest);
+    if (!kern) return fail(SS_ERR_CONFIG, "bad plan (ranks %d)", plan->ranks);
+    const RankArgs* args = static_cast<const RankArgs*>(plan->args_dev);
+    int per_rank = plan->blocks_per_rank;
+    int first = first_step ? 1 : 0;
+    void* params[] = {&args, &per_rank, &lr, &first};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(plan->ranks * per_rank));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, kern, params);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return fail(e == cudaErrorCooperativeLaunchTooLarge ? SS_ERR_CONFIG : SS_ERR_CUDA,
+                    "ss_colocated_step_f32: %s (%d ranks x %d blocks)", cudaGetErrorString(e), plan->ranks, per_rank);
+    }
+    return check_launch("ss_colocated_step_f32");
 }

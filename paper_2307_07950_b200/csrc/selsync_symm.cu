@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
     const int w = s_word;
     const bool sync = !s_timeout && w == SS_FLAG_SYNC;
     if (sync) {
-        average_shard<W>(a);
+        average_shard<W>(a, hw_blk());
         __threadfence_system();
     }
     __syncthreads();

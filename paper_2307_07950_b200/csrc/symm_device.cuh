@@ -4,6 +4,7 @@
 #pragma once
 
 #include "selsync_b200.h"
+#include "common.cuh"
 
 #include <cuda_runtime.h>
 
@@ -152,7 +153,13 @@ __device__ __forceinline__ float4 scale4(float4 v, float s) {
 // Mean over ranks of elements [e0, e1) by the threads of ONE block (tile work
 // of the overlapped sync step); e0 % 4 == 0, scalar tail when e1 % 4 != 0.
 template <int W>
-__device__ void average_block_range(const SymmArgs& a, int64_t e0, int64_t e1) {
+__device__ void average_block_range(const SymmArgs& a_in, int64_t e0, int64_t e1) {
+    // register copy of what the loops use (a_in may live in shared memory)
+    SymmArgs a;
+    a.mc = a_in.mc;
+    a.scale = a_in.scale;
+#pragma unroll
+    for (int r = 0; r < (W > 0 ? W : 1); ++r) a.bufs[r] = a_in.bufs[r];
     const int64_t v0 = e0 >> 2, v1 = e1 >> 2;
     if constexpr (W == 0) {
         int64_t i = v0 + threadIdx.x;
@@ -223,12 +230,20 @@ __device__ __forceinline__ void shard_range(const SymmArgs& a, int64_t* v0, int6
 // over W peers: all W loads of U vectors issued before any add (fixed rank
 // order => every rank's copy of a shard is bit-identical).
 template <int W, int UO = 0, int LS = 0>
-__device__ void average_shard(const SymmArgs& a) {
+__device__ void average_shard(const SymmArgs& a_in, VBlk vb) {
+    SymmArgs a;  // register copy of what the loops use (a_in may live in shared memory)
+    a.mc = a_in.mc;
+    a.scale = a_in.scale;
+    a.n = a_in.n;
+    a.rank = a_in.rank;
+    a.world = a_in.world;
+#pragma unroll
+    for (int r = 0; r < (W > 0 ? W : 1); ++r) a.bufs[r] = a_in.bufs[r];
     int64_t v0, v1;
     shard_range(a, &v0, &v1);
     const int64_t nvec = a.n >> 2;
-    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t tid = static_cast<int64_t>(vb.bid) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(vb.n) * blockDim.x;
     int64_t i = v0 + tid;
     if constexpr (W == 0) {
         constexpr int U = UO ? UO : 4;

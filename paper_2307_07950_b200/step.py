@@ -219,6 +219,8 @@ class SelSyncStep:
 
     def _enqueue_device_step(self, lr: float, stream) -> None:
         """K13+K2 -> C1 -> conditional C2, entirely on the device."""
+        if self.comm.backend == "colocated" and self.world > 1:
+            raise ConfigError("colocated ranks step together in one launch: use ColocatedSelSync.step")
         cfg = self.config
         ev = self._events(self.kernel_events)
         if ev:

@@ -160,7 +160,7 @@ def test_known_pass_one_tile_many_blocks(n):
     cfg = SelSyncConfig(delta=delta, warmup=warmup, smoothing=0.5, momentum=0.9, weight_decay=4e-4)
     col = ColocatedSelSync(torch.tensor(init, dtype=torch.float32, device=DEV), n, cfg, order="adaptive",
                            tile_elems=P, timeout_s=5.0)
-    assert col.max_blocks >= 64
+    assert col.blocks_per_rank >= 64
     for s in range(steps):
         col.set_grads([torch.from_numpy(O.synthetic_grad32(seed, r, s, P)).to(DEV) for r in range(n)])
         col.step(lr)
@@ -258,26 +258,31 @@ def test_steps_with_a_busy_device_stay_correct():
         params_close(col.params[r].double().cpu().numpy(), ref.finals[r])
 
 
-def test_grid_limit_and_split():
-    """The co-resident capacity the colocated ranks split; the P2P widths of
-    the step kernel are 1, 2, 4, 8 (other world sizes need multicast)."""
+def test_plan_splits_the_device_and_ranks_cannot_launch_alone():
+    """The N grids are one cooperative launch of N x G blocks (G capped so
+    all fit at once); a colocated rank never launches by itself (its kernel
+    would wait for peers that nothing guarantees to be running)."""
     cfg = SelSyncConfig(delta=0.05, warmup=2)
     col = ColocatedSelSync(torch.zeros(1 << 22, device=DEV), 4, cfg, order="update_first", timeout_s=2.0)
-    limit = col.ranks[0].symm.grid_limit(momentum=False, nesterov=False, grads=False)
-    assert limit >= torch.cuda.get_device_properties(DEV).multi_processor_count
-    assert col.max_blocks == limit // 4
+    sms = torch.cuda.get_device_properties(DEV).multi_processor_count
+    assert 1 <= col.blocks_per_rank and 4 * col.blocks_per_rank <= 8 * sms
     col.step(0.1)
     col.synchronize()
     with pytest.raises(ConfigError):
+        col.ranks[1].step_async(0.1)
+    with pytest.raises(ConfigError):
         ColocatedSelSync(torch.zeros(8, device=DEV), 3, cfg)
+    small = ColocatedSelSync(torch.zeros(1 << 22, device=DEV), 2, cfg, max_blocks=7)
+    assert small.blocks_per_rank == 7
+    small.step(0.1)
+    small.synchronize()
 
 
 def test_colocated_captured_steps_match_eager():
-    """Each rank's one-launch step captured as a CUDA graph (cooperative
-    kernel node) and replayed: same decisions and parameters as eager steps."""
-    c = MW.LARGE
+    """The colocated launch captured as a CUDA graph (a cooperative kernel
+    node) and replayed: same decisions and parameters as eager steps."""
     n, P, steps = 2, 262_144, 10
-    cfg = SelSyncConfig(delta=c["delta"], warmup=2, smoothing=0.5, momentum=0.9, weight_decay=4e-4)
+    cfg = SelSyncConfig(delta=0.05, warmup=2, smoothing=0.5, momentum=0.9, weight_decay=4e-4)
     init = torch.from_numpy(MW.large_init(3, P)).to(DEV)
     grads = [[torch.from_numpy(O.synthetic_grad32(3, r, s, P)).to(DEV) for r in range(n)] for s in range(steps)]
 
@@ -285,19 +290,11 @@ def test_colocated_captured_steps_match_eager():
         col = ColocatedSelSync(init, n, cfg, order="adaptive", tile_elems=4096, timeout_s=5.0)
         col.set_grads(grads[0])
         col.step(0.05)
-        col.synchronize()
-        graphs = None
-        if capture:
-            graphs = []
-            for r, st in enumerate(col.ranks):
-                with torch.cuda.stream(col.streams[r]):
-                    graphs.append(st.capture(0.05))
+        graph = col.capture(0.05) if capture else None
         for s in range(1, steps):
             col.set_grads(grads[s])
             if capture:
-                for r in range(n):
-                    with torch.cuda.stream(col.streams[r]):
-                        graphs[r].replay()
+                graph.replay()
             else:
                 col.step(0.05)
         col.synchronize()
@@ -307,3 +304,4 @@ def test_colocated_captured_steps_match_eager():
     for r in range(n):
         assert a.decisions(r) == b.decisions(r)
         torch.testing.assert_close(a.params[r], b.params[r], rtol=0, atol=0)
+    assert 0 < sum(a.decisions(0)[2:]) < steps - 2
