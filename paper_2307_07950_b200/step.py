@@ -33,8 +33,9 @@ Back ends (N > 1):
       issues NCCL allreduce-AVG on sync steps. ``fuse=False`` selects the
       pre-scale order instead: K1+K2, C1, K3 whose epilogue multiplies by 1/N
       when the agreed word says sync (the host read overlaps K3), allreduce-SUM.
-  Ranks sharing one GPU (``colocated.ColocatedSelSync``) use the symm back end
-  over same-device buffers, each rank on its own stream.
+  Ranks sharing one GPU (``colocated.ColocatedSelSync``) run the same step
+  kernels over same-device buffers, all ranks in ONE cooperative launch (rank
+  r's blocks are slice r of the grid).
 
 Gradient aggregation (aggregation="grads", :395-399): over symmetric memory
 the one-launch ``ss_step_symm_ga_f32`` (norm + vote, then per tile the

@@ -1,5 +1,5 @@
 """The multi-rank step kernels on ONE GPU: N colocated ranks (same-device
-peer buffers, one stream per rank, the device split between the N grids)
+peer buffers, the N grids as slices of one cooperative launch)
 against the reference's golden N-worker traces and the float64 oracle.
 
 These run the W = 2 / 4 / 8 instantiations of ``step_kernel`` /
