@@ -79,6 +79,8 @@ def parse():
                     help="elements per tile of the overlapped sync step (default: 4096 up to 2M params, else 16384)")
     ap.add_argument("--order", default="adaptive", choices=["update_first", "norm_first", "adaptive", "nan_safe"],
                     help="one-launch step order (flag-exchange fused): norm_first overlaps update and mean")
+    ap.add_argument("--early-vote", action="store_true",
+                    help="norm-first orders: the exact early vote (opt-in; A/B of the mean's start)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip the replayed golden decision patterns")
@@ -244,6 +246,7 @@ def workload_config(args, world):
         "collective": args.collective if world > 1 else "none (single rank)",
         "flag_exchange": args.flag_exchange if world > 1 else "none (single rank)",
         "step_order": args.order if world > 1 and args.flag_exchange == "fused" else "update_first",
+        "early_vote": bool(world > 1 and args.order in ("norm_first", "adaptive") and args.early_vote),
         "decision_mix": {"sync_frac": 0.5, "grad_scales": MIX_SCALES, "smoothing": 1.0, "delta": 0.3,
                          "warmup": 1},
         "parallelism": (f"dp{world} (SelSync replicas; vote + mean over "
@@ -305,7 +308,8 @@ def main():
         st = SelSyncStep(w, g, cfg, momentum_buffer=mom, group=comm, fuse=not args.no_fuse,
                          collective=args.collective if world > 1 else None,
                          flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
-                         trace_capacity=1 << 14, profile=not args.graph, order=args.order, tile_elems=args.tile)
+                         trace_capacity=1 << 14, profile=not args.graph, order=args.order, tile_elems=args.tile,
+                         early_vote=args.early_vote)
         return st
 
     captured = {}  # --graph: one CUDA graph per (step object, gradient buffer)

@@ -99,6 +99,15 @@ SS_API int ss_decide(const ss_signal_state* st_host, double delta, int32_t* sync
    No reference counterpart: it restates signal.py:101-107 one step ahead. */
 SS_API int ss_sync_known_ahead(const ss_signal_state* st_host, double delta, int32_t* known_out_host);
 
+/* *proven_out_host = 1 when observing ANY total >= lower next (lower: a
+   partial sum of the non-negative squares whose total is ||g||^2) is proven
+   to vote "sync" on the upward side (new EWMA >= previous): the exact early
+   vote of the norm-first step, which lets the mean start before the ||g||^2
+   sweep ends. Sound, not complete (downward jumps are never proven early).
+   No reference counterpart: it restates signal.py:64-107 for an interval. */
+SS_API int ss_sync_proven_early(const ss_signal_state* st_host, double lower, double delta,
+                                int32_t* proven_out_host);
+
 /* ---------------- device hot path (sm_100a) ---------------- */
 
 /* bytes of scratch (block partials + arrival counter) any kernel below needs;
@@ -203,6 +212,9 @@ SS_API int ss_replica_flag_max_i32(int32_t* const* words_host, int32_t count, vo
    addresses valid in this process. The signal regions hold 3*world uint64
    slots (ss_symm_signal_bytes: votes double-buffered by step parity + end-
    barrier tags) and must start zeroed on every rank. */
+#define SS_ORDER_MODE_MASK 0x3          /* order_mode bits selecting order 0-3 */
+#define SS_ORDER_EARLY_VOTE 0x10        /* order_mode flag: the exact early vote (opt-in) */
+
 typedef struct ss_symm_group {
     float* bufs[SS_SYMM_MAX_RANKS];     /* rank r's flat fp32 buffer */
     uint64_t* pads[SS_SYMM_MAX_RANKS];  /* rank r's signal region */
@@ -233,6 +245,12 @@ typedef struct ss_symm_group {
        decision is sync before ||g||^2 is known (ss_sync_known_ahead); a rank
        whose update tile holds a NaN poisons the mean of that tile on its owner,
        so a NaN never reaches another rank's buffer.
+       order_mode | SS_ORDER_EARLY_VOTE (orders 1/2 outside the known pass, opt-in):
+       the exact early vote -- the ||g||^2 sweep reports a running sum in 8
+       chunks, and once that lower bound proves the vote sync
+       (ss_sync_proven_early: an upward jump) an early tag lets every rank's
+       mean tickets start before the sweep ends; a NaN update tile then
+       poisons its mean as in the known pass. Measured: no gain.
        All orders compute identical parameters. Orders 1-3 need the fields below. */
     int32_t order_mode;
     float order_threshold;
@@ -249,7 +267,7 @@ typedef struct ss_symm_group {
 } ss_symm_group;
 
 /* bytes of each rank's signal region (2 x world vote slots + world done slots + world
-   poison slots, uint64 each) */
+   poison slots + world early-sync slots, uint64 each) */
 SS_API int ss_symm_signal_bytes(int32_t world, int64_t* bytes_host);
 /* layout check for FFI mirrors of ss_symm_group: byte offsets of its fields in
    declaration order, then sizeof(ss_symm_group); *count_host = entries written

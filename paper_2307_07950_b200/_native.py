@@ -64,6 +64,7 @@ class TraceRowC(Structure):
 
 
 SYMM_MAX_RANKS = 16
+ORDER_EARLY_VOTE = 0x10  # SS_ORDER_EARLY_VOTE: order_mode flag, the exact early vote (opt-in)
 
 
 class SymmGroupC(Structure):
@@ -125,6 +126,7 @@ _SIGS = {
     "ss_relative_change": ([POINTER(SignalStateC), POINTER(c_double)], c_int),
     "ss_decide": ([POINTER(SignalStateC), c_double, POINTER(c_int32)], c_int),
     "ss_sync_known_ahead": ([POINTER(SignalStateC), c_double, POINTER(c_int32)], c_int),
+    "ss_sync_proven_early": ([POINTER(SignalStateC), c_double, c_double, POINTER(c_int32)], c_int),
     "ss_workspace_bytes": ([POINTER(c_int64)], c_int),
     "ss_workspace_reset": ([_P, _P], c_int),
     "ss_norm_sq_f32": ([_P, c_int64, _P, _P, _P], c_int),

@@ -174,6 +174,13 @@ class SymmetricView:
         self.group_c = g
         self.group_ref = ctypes.byref(g)
 
+    def set_early_vote(self, on: bool) -> None:
+        """Exact early vote of the norm-first orders (opt-in): the
+        mean starts once a running lower bound of ||g||^2 proves the vote sync."""
+        from . import _native as N
+
+        self.group_c.order_mode = ORDERS[self.order] | (N.ORDER_EARLY_VOTE if on else 0)
+
     def sync_(self, word: torch.Tensor, ws_ptr: int, *, exchange: bool, stream: int) -> None:
         from . import _native as N
 

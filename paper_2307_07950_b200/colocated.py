@@ -166,7 +166,7 @@ class ColocatedSelSync:
     def __init__(self, init_params: torch.Tensor, n_ranks: int, config: SelSyncConfig, *,
                  order: str = "adaptive", order_threshold: float = 0.2, tile_elems: Optional[int] = None,
                  timeout_s: float = 10.0, max_blocks: int = 0, trace_capacity: int = 4096,
-                 nan_safe: bool = False):
+                 nan_safe: bool = False, early_vote: bool = False):
         from .step import SelSyncStep
 
         if not isinstance(init_params, torch.Tensor) or not init_params.is_cuda:
@@ -186,7 +186,7 @@ class ColocatedSelSync:
             st = SelSyncStep(init, torch.zeros_like(p0), config, group=self.world.group(r), collective="symm",
                              flag_exchange="fused", order=order, order_threshold=order_threshold,
                              tile_elems=tile_elems, timeout_s=timeout_s, trace_capacity=trace_capacity,
-                             nan_safe=nan_safe)
+                             nan_safe=nan_safe, early_vote=early_vote)
             self.ranks.append(st)
         grads = config.aggregation == "grads"
         table = (N.RankStepC * self.n)()

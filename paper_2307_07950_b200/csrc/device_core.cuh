@@ -35,8 +35,9 @@ __host__ __device__ inline Workspace ws_view(void* ws) {
     return Workspace{reinterpret_cast<unsigned int*>(b), reinterpret_cast<double*>(b + kWsHeader)};
 }
 // header: norm arrival counter at 0, exchange arrival counter at 64, ticket at
-// 128, the update-first step's decision broadcast at 192, the one-launch
-// step's block-start counter at 224; then the partials
+// 128, the early vote's running sum at 160 and posted tag at 176, the
+// update-first step's decision broadcast at 192, the one-launch step's
+// block-start counter at 224; then the partials
 constexpr int64_t kWsBytes = kWsHeader + 8 * kMaxGrid;
 
 // ------------------------------------------- exact IEEE scalar arithmetic
@@ -136,6 +137,25 @@ __host__ __device__ inline bool sync_known_ahead_core(int64_t step_count, int32_
     return delta == 0.0 && ewma_current - ewma_current == 0.0;  // finite
 }
 
+// Exact early vote: `lower` is a partial sum of the non-negative terms whose
+// total the finishing block will observe (the same block partials, a subset,
+// summed in another order). If observing a value a little below `lower`
+// already votes sync on the upward side (new EWMA >= previous), then so does
+// the total: every operation of observe / relative_change rounds monotonically
+// in x there, and the margin (1e-9 relative) covers the two summation orders
+// (their difference is < 1e-12 relative for <= 8192 partials). Downward
+// jumps are never proven early (they need an upper bound). NaN / inf-times-0
+// give false. tests/test_signal_api.py checks soundness against the scalar
+// vote of every total >= lower.
+__host__ __device__ inline bool sync_proven_early_core(const ss_signal_state* st, double lower, double delta) {
+    if (!(lower >= 0.0) || st->step_count < 1 || !(st->smoothing > 0.0)) return false;
+    ss_signal_state s = *st;
+    if (observe_core(&s, mul_rn(lower, 1.0 - 1e-9))) return false;
+    if (s.step_count <= s.warmup) return true;
+    if (!(s.ewma_current >= s.ewma_previous)) return false;
+    return rel_change_core(s.ewma_previous, s.ewma_current) >= delta;
+}
+
 // K2 body: one thread. Writes the flag word and the trace row.
 __device__ void signal_step_dev(ss_signal_state* st, double x, double delta, int32_t* word,
                                 ss_trace_row* trace, int32_t cap) {
@@ -212,6 +232,10 @@ __device__ __forceinline__ double sq4(float4 v, double acc) {
     acc = fma(static_cast<double>(v.z), static_cast<double>(v.z), acc);
     acc = fma(static_cast<double>(v.w), static_cast<double>(v.w), acc);
     return acc;
+}
+
+__device__ __forceinline__ bool is_nan4(float4 v) {
+    return (v.x != v.x) | (v.y != v.y) | (v.z != v.z) | (v.w != v.w);
 }
 
 // block sum; the value is valid in thread 0 only (fixed order => deterministic)
@@ -292,6 +316,33 @@ __device__ __forceinline__ double norm_pass(const float* __restrict__ g, int64_t
     for (int64_t j = head + 4 * nvec + tid; j < n; j += stride) acc = fma((double)g[j], (double)g[j], acc);
     return acc;
 }
+// Chunk c of C of the same sweep (the float4 vectors split into C contiguous
+// ranges, each grid-strided; the head scalars go with chunk 0, the tail with
+// chunk C - 1), accumulated onto acc.
+template <int U>
+__device__ __forceinline__ double norm_chunk(const float* __restrict__ g, int64_t n, int64_t head, VBlk vb, int c,
+                                             int C, double acc) {
+    const int64_t tid = static_cast<int64_t>(vb.bid) * blockDim.x + threadIdx.x;
+    const int64_t stride = static_cast<int64_t>(vb.n) * blockDim.x;
+    const float* gb = g + head;
+    const int64_t nvec = (n - head) >> 2;
+    if (c == 0)
+        for (int64_t i = tid; i < head; i += stride) acc = fma((double)g[i], (double)g[i], acc);
+    const int64_t v0 = nvec * c / C, v1 = nvec * (c + 1) / C;
+    int64_t i = v0 + tid;
+    for (; i + (U - 1) * stride < v1; i += U * stride) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_cs4(gb + 4 * (i + u * stride));
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = sq4(v[u], acc);
+    }
+    for (; i < v1; i += stride) acc = sq4(ld_cs4(gb + 4 * i), acc);
+    if (c == C - 1)
+        for (int64_t j = head + 4 * nvec + tid; j < n; j += stride) acc = fma((double)g[j], (double)g[j], acc);
+    return acc;
+}
+
 template <int U>
 __device__ __forceinline__ double norm_pass(const float* __restrict__ g, int64_t n, int64_t head) {
     return norm_pass<U>(g, n, head, hw_blk());
@@ -439,7 +490,8 @@ __device__ __forceinline__ double sgd_pass(const SgdArgs& a) {
 // the overlapped sync step). Requires 16-byte-aligned streams (head == 0) and
 // e0 % 4 == 0; a scalar tail is handled when e1 is not a multiple of 4.
 // NORM: also return this thread's fp64 partial of ||g||^2 over the range.
-template <bool MOM, bool NEST, int U = 2, bool G_L2 = false, bool NORM = false>
+// NANF: return 1 when this thread met a NaN gradient element, else 0.
+template <bool MOM, bool NEST, int U = 2, bool G_L2 = false, bool NORM = false, bool NANF = false>
 __device__ __forceinline__ double sgd_block_range(const SgdArgs& a_in, int64_t e0, int64_t e1) {
     const SgdArgs a = a_in;  // register copy (see sgd_pass)
     // G_L2: read g through L2 only (it was just rewritten by peers over NVLink)
@@ -448,6 +500,7 @@ __device__ __forceinline__ double sgd_block_range(const SgdArgs& a_in, int64_t e
     // flight than in the whole-grid K13 sweep (where U = 1 is best)
     const float s = 1.0f;
     double acc = 0.0;
+    bool bad = false;
     const int64_t v0 = e0 >> 2, v1 = e1 >> 2;
     const int64_t bs = blockDim.x;
     int64_t i = v0 + threadIdx.x;
@@ -464,6 +517,7 @@ __device__ __forceinline__ double sgd_block_range(const SgdArgs& a_in, int64_t e
         for (int u = 0; u < U; ++u) {
             const int64_t k = 4 * (i + u * bs);
             if (NORM) acc = sq4(gv[u], acc);
+            if (NANF) bad |= is_nan4(gv[u]);
             float4 mm = MOM ? mv[u] : make_float4(0.f, 0.f, 0.f, 0.f);
             sgd_elem<MOM, NEST>(wv[u].x, gv[u].x, mm.x, a, s);
             sgd_elem<MOM, NEST>(wv[u].y, gv[u].y, mm.y, a, s);
@@ -479,6 +533,7 @@ __device__ __forceinline__ double sgd_block_range(const SgdArgs& a_in, int64_t e
         float4 wv = ld_cs4(a.w + k);
         float4 mm = MOM ? ld_cs4(a.m + k) : make_float4(0.f, 0.f, 0.f, 0.f);
         if (NORM) acc = sq4(gv, acc);
+        if (NANF) bad |= is_nan4(gv);
         sgd_elem<MOM, NEST>(wv.x, gv.x, mm.x, a, s);
         sgd_elem<MOM, NEST>(wv.y, gv.y, mm.y, a, s);
         sgd_elem<MOM, NEST>(wv.z, gv.z, mm.z, a, s);
@@ -491,10 +546,12 @@ __device__ __forceinline__ double sgd_block_range(const SgdArgs& a_in, int64_t e
         float w = a.w[j], g = G_L2 ? __ldcg(a.g + j) : a.g[j];
         float m = MOM ? a.m[j] : 0.0f;
         if (NORM) acc = fma(static_cast<double>(g), static_cast<double>(g), acc);
+        if (NANF) bad |= g != g;
         sgd_elem<MOM, NEST>(w, g, MOM ? m : mdummy, a, s);
         a.w[j] = w;
         if (MOM) a.m[j] = m;
     }
+    if (NANF) return bad ? 1.0 : 0.0;
     return acc;
 }
 

@@ -277,6 +277,14 @@ int ss_sync_known_ahead(const ss_signal_state* st, double delta, int32_t* known_
     return SS_OK;
 }
 
+int ss_sync_proven_early(const ss_signal_state* st, double lower, double delta, int32_t* proven_out) {
+    if (!st || !proven_out) return fail(SS_ERR_CONFIG, "null argument");
+    int rc = check_delta_impl(delta);
+    if (rc) return rc;
+    *proven_out = sync_proven_early_core(st, lower, delta) ? 1 : 0;
+    return SS_OK;
+}
+
 int ss_workspace_bytes(int64_t* bytes) {
     if (!bytes) return fail(SS_ERR_CONFIG, "null output");
     *bytes = kWsBytes;

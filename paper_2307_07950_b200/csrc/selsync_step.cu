@@ -65,12 +65,22 @@ struct OverlapArgs {
     int64_t tile;
     int64_t n_tiles;
     int lag;                   // groups between an update ticket and the owner's mean ticket
+    int early;                 // exact early vote enabled (norm-first orders without the known pass)
     unsigned long long* ticket;
     uint64_t* dbg;             // optional per-ticket timeline: {kind << 48 | tile, t0, t_ready, t_end}
     int64_t dbg_cap;
     double* tile_norm;         // known-sync pass: ||g||^2 partial per tile (NULL: pass disabled)
     unsigned int* started;     // blocks that took this launch's order snapshot (workspace, self-resetting)
+    double* running;           // early vote: running sum of the block partials (workspace, self-resetting)
+    uint64_t* early_posted;    // early vote: seq of the last step this rank posted an early sync tag for
 };
+
+#ifndef SS_LAG_DIV
+#define SS_LAG_DIV 1
+#endif
+
+constexpr int kEarlySync = -3;  // vote_or_early: a peer proved the step sync before its sweep ended
+constexpr int kEarlyChunks = 8;  // the early vote's ||g||^2 sweep reports its running sum this often
 
 // order bits of one launch, decided once per block at kernel start
 constexpr int kNormFirst = 1, kKnown = 2, kSafe = 4;
@@ -153,6 +163,33 @@ __device__ int agreed_vote(const SymmArgs& s, uint64_t seq) {
     return w;
 }
 
+// Wait for the N final votes of step `seq` (returns their MAX, -1 on a
+// timeout) or for an early sync tag from any rank, whichever comes first
+// (returns kEarlySync). An early tag proves its rank's final vote is sync (or
+// an error word), so the agreed word is >= SS_FLAG_SYNC: the mean may start.
+__device__ int vote_or_early(const SymmArgs& s, uint64_t seq) {
+    const uint64_t t0 = now_ns();
+    for (;;) {
+        int w = 0, have = 0;
+        for (int j = 0; j < s.world; ++j) {
+            const uint64_t t = ld_acquire_sys(vote_slot(s, s.rank, seq, j));
+            if ((t >> 32) == seq) {
+                ++have;
+                const int wj = static_cast<int>(static_cast<uint32_t>(t));
+                w = wj > w ? wj : w;
+            }
+        }
+        if (have == s.world) return w;
+        for (int j = 0; j < s.world; ++j)
+            if (ld_acquire_sys(early_slot(s, s.rank, j)) == seq) return kEarlySync;
+        if (now_ns() - t0 > s.timeout_ns) {
+            atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
+            return -1;
+        }
+        __nanosleep(64);
+    }
+}
+
 // Known-sync pass: called by every thread of the block that just finished an
 // update tile (its ||g||^2 partial is in tile_norm). The block finishing the
 // last tile of this rank reduces the partials in tile order (deterministic),
@@ -194,7 +231,11 @@ __device__ __forceinline__ bool sync_known_ahead(const Finish& f) {
 
 // This launch's order, read by thread 0 of every block from state that only
 // the last block of the PREVIOUS launch (predictor) or a K2 that waits for
-// every block's arrival here (known pass) writes: all blocks agree.
+// every block's arrival here (known pass) writes: all blocks agree. Only the
+// known pass runs K2 before every block has arrived at the norm counter, so
+// only a known snapshot counts itself in `started` (no 1-per-block atomic on
+// other steps): K2 of the known pass waits for all of them, hence every block
+// reads the state before K2 changes it and takes the known snapshot too.
 __device__ int order_snapshot(const Finish& f, const OverlapArgs& o) {
     __shared__ int s_order;
     if (threadIdx.x == 0) {
@@ -202,8 +243,10 @@ __device__ int order_snapshot(const Finish& f, const OverlapArgs& o) {
         const bool nf = known || o.mode == 1 || o.mode == 3 ||
                         (o.mode == 2 && predicted_sync(o.predictor) >= o.threshold);
         s_order = (nf ? kNormFirst : 0) | (known ? kKnown : 0) | (o.mode == 3 ? kSafe : 0);
-        __threadfence();  // the state reads above complete before the arrival below
-        atomicAdd(o.started, 1u);
+        if (known) {
+            __threadfence();  // the state reads above complete before the arrival below
+            atomicAdd(o.started, 1u);
+        }
     }
     __syncthreads();
     return s_order;
@@ -227,13 +270,45 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     // ||g||^2 then comes from the update tiles themselves (no separate sweep)
     // and the vote is still exchanged at the end, for the trace, the EWMA and
     // the error bits.
-    if (threadIdx.x == 0) s_vote = known ? SS_FLAG_SYNC : -2;
+    // early: the exact early vote -- each block adds its ||g||^2 partial to a
+    // running sum; once that lower bound proves the vote sync (upward jump,
+    // sync_proven_early_core) the block posts an early sync tag to every rank
+    // and the mean tickets start before the sweep ends. A NaN tile then
+    // poisons its mean (as in the known pass): the final vote comes later.
+    const bool early = o.early && !known && !safe;
+    __shared__ bool s_early;
+    if (threadIdx.x == 0) {
+        s_vote = known ? SS_FLAG_SYNC : -2;
+        s_early = false;
+    }
     // ---- phase 1: ||g||^2 by the whole grid (full-speed sweep); the last block
     //      to arrive reduces the partials in a fixed order, runs K2 and posts the
     //      vote. Nobody waits here: blocks go straight on to the update tickets.
     if (!known) {
         Workspace ws = ws_view(f.ws);
-        const double bsum = block_sum(norm_pass<4>(a.g, a.n, a.head, vb));
+        double bsum;
+        if (early) {
+            // the sweep in kEarlyChunks grid-strided chunks: after each one every
+            // block adds what it summed to the running lower bound, which so grows
+            // with the sweep instead of arriving all at once at its end
+            double acc = 0.0, prev = 0.0;
+            for (int c = 0; c < kEarlyChunks; ++c) {
+                acc = norm_chunk<4>(a.g, a.n, a.head, vb, c, kEarlyChunks, acc);
+                const double cum = block_sum(acc);
+                if (threadIdx.x == 0) {
+                    const double lower = atomicAdd(o.running, cum - prev) + (cum - prev);
+                    prev = cum;
+                    if (ld_relaxed_gpu(o.early_posted) != seq && sync_proven_early_core(f.st, lower, f.delta)) {
+                        *reinterpret_cast<volatile uint64_t*>(o.early_posted) = seq;
+                        for (int j = 0; j < N; ++j) st_release_sys(early_slot(s, j, s.rank), seq);
+                        if (o.dbg) o.dbg[4 * o.dbg_cap + 3] = now_ns();
+                    }
+                }
+            }
+            bsum = prev;
+        } else {
+            bsum = block_sum(norm_pass<4>(a.g, a.n, a.head, vb));
+        }
         if (threadIdx.x == 0) {
             ws.partials[vb.bid] = bsum;
             __threadfence();
@@ -247,6 +322,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
             v = block_sum(v);
             if (threadIdx.x == 0) {
                 *ws.counter = 0u;
+                if (early) *o.running = 0.0;  // every block has added its partial
                 signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
                 const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
                 __threadfence_system();
@@ -291,8 +367,10 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                     if (safe && (s_vote & ~SS_FLAG_SYNC) != 0) {
                         // counted all the same: tile counts advance by N every norm-first step
                     } else if (!known) {
-                        sgd_block_range<MOM, NEST>(a, e0, e1);
-                        __syncthreads();
+                        const double bad = sgd_block_range<MOM, NEST, 2, false, false, true>(a, e0, e1);
+                        // the barrier orders the block's stores before the count below;
+                        // a NaN in this tile poisons its mean if the early vote runs it
+                        if (__syncthreads_or(bad != 0.0) && early && threadIdx.x == 0) post_poison(s, seq);
                     } else {
                         // block_sum's barriers also order the block's stores
                         const double ts = block_sum(sgd_block_range<MOM, NEST, 1, false, true>(a, e0, e1));
@@ -316,8 +394,12 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                 const int64_t t = m * N + s.rank;
                 if (m >= 0 && t < T) {
                     if (threadIdx.x == 0) {
-                        if (s_vote == -2) s_vote = agreed_vote(s, seq);
-                        bool go = s_vote == SS_FLAG_SYNC;
+                        if (s_vote == -2 && !s_early) {
+                            const int r = early ? vote_or_early(s, seq) : agreed_vote(s, seq);
+                            if (r == kEarlySync) s_early = true;
+                            else s_vote = r;
+                        }
+                        bool go = s_early || s_vote == SS_FLAG_SYNC;
                         if (go) {
                             const uint64_t t0 = now_ns();
                             while (static_cast<int32_t>(ld_acquire_sys_u32(o.cnt[s.rank] + t) - target) < 0) {
@@ -330,7 +412,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                             }
                             // known pass: a NaN met by any rank before its count
                             // of this tile stops the mean here (acquired above)
-                            if (go && known && poisoned(s, seq)) go = false;
+                            if (go && (known || s_early) && poisoned(s, seq)) go = false;
                         }
                         s_go = go;
                     }
@@ -361,7 +443,8 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
         *f.word = w;
         if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
         if (o.mode == 2) predictor_update(o.predictor, w);
-        if (w == SS_FLAG_SYNC || known) end_barrier(s, seq);  // known: the mean ran in any case
+        // known: the mean ran in any case; early: it may have run on an error step
+        if (w == SS_FLAG_SYNC || known || (early && w > 0)) end_barrier(s, seq);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 5] = now_ns();
         *o.ticket = 0ull;
         *o.epoch = epoch;
@@ -403,7 +486,6 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
         v = block_sum(v);
         if (threadIdx.x == 0) {
             *ws.counter = 0u;
-            *o.started = 0u;  // every block has arrived: all took their snapshot
             signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
             const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
             __threadfence_system();
@@ -506,7 +588,9 @@ __device__ __forceinline__ void ga_body(const SgdArgs& a, const Finish& f, const
         }
     }
     __syncthreads();
-    // every ticket needs the branch: the agreed vote (all ranks finished their sweep)
+    // every ticket needs the branch: the agreed vote (all ranks finished their
+    // sweep -- the means overwrite the gradients the sweeps read, so there is
+    // no early vote here)
     if (threadIdx.x == 0) s_vote = agreed_vote(s, seq);
     __syncthreads();
     const bool sync = s_vote == SS_FLAG_SYNC;
@@ -635,7 +719,8 @@ int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, i
     f.total_blocks = grid;
     // norm-first pass: the in-flight window is ~grid tickets = grid / (N + 1)
     // groups; the mean of a tile is scheduled one window after its update
-    o.lag = grid / (sa.world + 1) + 2;
+    // (SS_LAG_DIV: A/B builds of a shorter lag)
+    o.lag = grid / (sa.world + 1) / SS_LAG_DIV + 2;
     return launch_coop(step_kernel<MOM, NEST, W>, grid, stream, "ss_step_symm_f32", a, f, sa, o);
 }
 
@@ -700,7 +785,10 @@ int build_rank_args(bool ga, float* w, float* g, float* m, int64_t n, float lr, 
     OverlapArgs o{};
     o.dbg = grp->debug_events;
     o.dbg_cap = grp->debug_events ? grp->debug_cap : 0;
-    o.mode = ga ? 0 : grp->order_mode;
+    o.mode = ga ? 0 : (grp->order_mode & SS_ORDER_MODE_MASK);
+    o.early = (!ga && (grp->order_mode & SS_ORDER_EARLY_VOTE)) ? 1 : 0;
+    o.running = reinterpret_cast<double*>(static_cast<char*>(ws) + 160);
+    o.early_posted = reinterpret_cast<uint64_t*>(static_cast<char*>(ws) + 176);
     o.threshold = grp->order_threshold;
     o.started = reinterpret_cast<unsigned int*>(static_cast<char*>(ws) + 224);
     o.ticket = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 128);
@@ -712,7 +800,9 @@ int build_rank_args(bool ga, float* w, float* g, float* m, int64_t n, float lr, 
             return fail(SS_ERR_CONFIG, "gradient aggregation needs epoch and a tile size (multiple of 4)");
     } else {
         if (grp->bufs[grp->rank] != w) return fail(SS_ERR_CONFIG, "w must be this rank's symmetric buffer");
-        if (o.mode < 0 || o.mode > 3) return fail(SS_ERR_CONFIG, "order_mode must be 0, 1, 2 or 3, got %d", o.mode);
+        if ((grp->order_mode & ~(SS_ORDER_MODE_MASK | SS_ORDER_EARLY_VOTE)) != 0 || o.mode > 3)
+            return fail(SS_ERR_CONFIG, "order_mode must be 0, 1, 2 or 3 (| SS_ORDER_EARLY_VOTE), got %d",
+                        grp->order_mode);
         if (o.mode != 0) {
             if (a.head != 0) return fail(SS_ERR_CONFIG, "norm-first order needs 16-byte aligned w, g, m");
             if (!grp->epoch || !grp->predictor || grp->tile_elems <= 0 || (grp->tile_elems & 3))

@@ -38,10 +38,17 @@ using ss_internal::fail;
 
 namespace {
 
-constexpr int kThreads = 512;
+// block shape of the standalone exchange (A/B builds: SS_SYMM_THREADS / SS_SYMM_MINB)
+#ifndef SS_SYMM_THREADS
+#define SS_SYMM_THREADS 512
+#endif
+#ifndef SS_SYMM_MINB
+#define SS_SYMM_MINB 2
+#endif
+constexpr int kThreads = SS_SYMM_THREADS;
 
 template <int W>
-__global__ void __launch_bounds__(kThreads, 2) symm_sync_kernel(SymmArgs a) {
+__global__ void __launch_bounds__(kThreads, SS_SYMM_MINB) symm_sync_kernel(SymmArgs a) {
     __shared__ int s_word;
     __shared__ bool s_timeout;
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(a.seq)) + 1;
@@ -139,7 +146,7 @@ int ss_symm_group_layout(int64_t* offsets, int32_t cap, int32_t* count) {
 int ss_symm_signal_bytes(int32_t world, int64_t* bytes) {
     if (!bytes) return fail(SS_ERR_CONFIG, "null output");
     if (world < 1 || world > kMaxRanks) return fail(SS_ERR_CONFIG, "world size must be in [1, %d], got %d", kMaxRanks, world);
-    *bytes = 4 * static_cast<int64_t>(world) * static_cast<int64_t>(sizeof(uint64_t));
+    *bytes = 5 * static_cast<int64_t>(world) * static_cast<int64_t>(sizeof(uint64_t));
     return SS_OK;
 }
 

@@ -46,19 +46,41 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
     return v;
 }
 
+// NVLS tuning (A/B builds, tools/ab_build.sh): SS_NVLS_WEAK=1 uses .weak
+// instead of .relaxed.sys; SS_NVLS_U sets the 16-byte vectors per thread in flight
+#ifndef SS_NVLS_WEAK
+#define SS_NVLS_WEAK 0
+#endif
+#ifndef SS_NVLS_U
+#define SS_NVLS_U 4
+#endif
+
 __device__ __forceinline__ float4 mm_ld_reduce_add4(const float* p) {
     float4 v;
+#if SS_NVLS_WEAK
+    asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
+#else
     asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "l"(p)
                  : "memory");
+#endif
     return v;
 }
 
 __device__ __forceinline__ void mm_st4(float* p, float4 v) {
+#if SS_NVLS_WEAK
+    asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+#else
     asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
                  "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
+#endif
 }
 
 __device__ __forceinline__ float mm_ld_reduce_add1(const float* p) {
@@ -129,6 +151,11 @@ __device__ __forceinline__ uint64_t* done_slot(const SymmArgs& a, int owner, int
 // tile of the known-sync pass, whose mean runs before the vote is in
 __device__ __forceinline__ uint64_t* poison_slot(const SymmArgs& a, int owner, int from) {
     return a.pads[owner] + 3 * a.world + from;
+}
+// early sync tags (seq of the step): rank `from`'s running lower bound of
+// ||g||^2 proved its vote sync before its sweep ended (exact early vote)
+__device__ __forceinline__ uint64_t* early_slot(const SymmArgs& a, int owner, int from) {
+    return a.pads[owner] + 4 * a.world + from;
 }
 
 // peer load / store flavours of the P2P mean (tuning: SS_P2P_VARIANT)
@@ -246,7 +273,7 @@ __device__ void average_shard(const SymmArgs& a_in, VBlk vb) {
     const int64_t stride = static_cast<int64_t>(vb.n) * blockDim.x;
     int64_t i = v0 + tid;
     if constexpr (W == 0) {
-        constexpr int U = UO ? UO : 4;
+        constexpr int U = UO ? UO : SS_NVLS_U;
         for (; i + (U - 1) * stride < v1; i += U * stride) {
             float4 v[U];
 #pragma unroll

@@ -119,6 +119,18 @@ def sync_known_ahead(state: GradSignalState, threshold: DeltaThreshold) -> bool:
     return bool(out.value)
 
 
+def sync_proven_early(state: GradSignalState, threshold: DeltaThreshold, lower: float) -> bool:
+    """True when observing ANY norm >= ``lower`` next is proven to decide
+    "sync" on the upward side (new EWMA >= previous): the exact early vote the
+    norm-first step posts from a running partial sum of ||g||^2 before the
+    sweep ends. Sound, not complete. Not in the reference (it restates
+    signal.py:64-107 over an interval)."""
+    c = state.to_c()
+    out = ctypes.c_int32(0)
+    N.check(N.LIB.ss_sync_proven_early(ctypes.byref(c), float(lower), float(threshold.delta), ctypes.byref(out)))
+    return bool(out.value)
+
+
 def replay_decisions(deltas, warmup: int, delta: float) -> int:
     """Count sync decisions of a recorded Delta trace at one threshold
     (signal.py:110-124); entries recorded during warmup are None."""

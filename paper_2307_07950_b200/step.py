@@ -89,6 +89,7 @@ class SelSyncStep:
         multicast="auto",
         nan_safe: bool = False,
         max_blocks: int = 0,
+        early_vote: bool = False,
     ):
         if not isinstance(config, SelSyncConfig):
             raise ConfigError("config must be a SelSyncConfig")
@@ -158,6 +159,7 @@ class SelSyncStep:
                                                  order=order, order_threshold=order_threshold,
                                                  tile_elems=tile_elems, use_multicast=multicast,
                                                  max_blocks=max_blocks)
+            self.symm.set_early_vote(early_vote)
             if config.aggregation == "grads":
                 # the exchanged vector is the gradient: it lives in symmetric memory
                 self.symm.buf.copy_(grads)

@@ -305,3 +305,50 @@ def test_colocated_captured_steps_match_eager():
         assert a.decisions(r) == b.decisions(r)
         torch.testing.assert_close(a.params[r], b.params[r], rtol=0, atol=0)
     assert 0 < sum(a.decisions(0)[2:]) < steps - 2
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("order,agg", [("norm_first", "params"), ("adaptive", "params")])
+def test_early_vote_fires_on_upward_jumps_and_changes_nothing(n, order, agg):
+    """Exact early vote (norm-first orders): a block whose running lower bound
+    of ||g||^2 proves the vote sync posts an early tag and the mean tickets
+    start before the sweep ends. Gradients scaled [1, 1, 1.5, 1.5] cycled
+    (smoothing 1, delta 0.3: local / up / local / down): the tag must appear on
+    upward sync steps only, never on local steps, and the run must be
+    bit-identical to the same run with the early vote off (and match the
+    float64 oracle)."""
+    P, steps, seed, lr = 1 << 20, 16, 41, 0.05
+    scales = [1.0, 1.0, 1.5, 1.5]
+    cfg = SelSyncConfig(delta=0.3, warmup=1, smoothing=1.0, momentum=0.9, weight_decay=4e-4, aggregation=agg)
+    init = torch.from_numpy(MW.large_init(seed, P)).to(DEV)
+    base = [torch.from_numpy(O.synthetic_grad32(seed, r, 0, P)).to(DEV) for r in range(n)]
+
+    def run(early):
+        col = ColocatedSelSync(init, n, cfg, order=order, tile_elems=16384, timeout_s=10.0, early_vote=early)
+        fired = []
+        for s in range(steps):
+            col.set_grads([b * scales[s % 4] for b in base])
+            col.step(lr)
+            col.synchronize()
+            tags = col.world.pads[:, 4 * n:5 * n].cpu()
+            fired.append(bool((tags == s + 1).any()))
+        return col, fired
+
+    on, fired = run(True)
+    off, fired_off = run(False)
+    dec = on.decisions(0)
+    assert not any(fired_off)
+    assert any(fired), "no early vote on an upward jump"
+    for s in range(steps):
+        if fired[s]:
+            assert dec[s] == 1 and scales[s % 4] > scales[(s - 1) % 4], (s, dec)
+    for r in range(n):
+        assert on.decisions(r) == off.decisions(r)
+        torch.testing.assert_close(on.params[r], off.params[r], rtol=0, atol=0)
+        torch.testing.assert_close(on.ranks[r].momentum, off.ranks[r].momentum, rtol=0, atol=0)
+    ref = O.simulate_selsync(init.double().cpu().numpy(), n, steps,
+                             lambda w, s, _p: (base[w].cpu().numpy() * np.float32(scales[s % 4])).astype(np.float64),
+                             delta=0.3, warmup=1, smoothing=1.0, lr=lr, momentum=0.9, weight_decay=4e-4,
+                             aggregation=agg)
+    assert_trace_parity(dec, ref.decision, ref.delta_g, 0.3, 1)
+    params_close(on.params[0].double().cpu().numpy(), ref.finals[0])

@@ -1,5 +1,6 @@
 """Timeline of the overlapped (norm-first) sync step: per-ticket timestamps
-from the device, summarised per rank (torchrun, one rank per GPU)."""
+from the device, summarised per rank (torchrun, one rank per GPU).
+Args: P, tile, mode (known | up | down | up-early)."""
 import os
 import sys
 from pathlib import Path
@@ -21,11 +22,24 @@ dev = torch.device("cuda", local)
 dist.init_process_group("nccl", device_id=dev)
 w = torch.randn(P, device=dev)
 g = torch.randn(P, device=dev)
-cfg = SelSyncConfig(delta=0.0, warmup=1, momentum=0.9, weight_decay=4e-4)
-st = SelSyncStep(w, g, cfg, order="norm_first", tile_elems=tile)
+# mode: known (delta = 0: the known-sync pass) | up / down (delta 0.3, smoothing 1:
+# a sync step on an upward / downward jump of ||g||^2 after local steps) |
+# up-early (the same upward step with the opt-in exact early vote)
+mode = sys.argv[3] if len(sys.argv) > 3 else "known"
+if mode == "known":
+    cfg = SelSyncConfig(delta=0.0, warmup=1, momentum=0.9, weight_decay=4e-4)
+else:
+    cfg = SelSyncConfig(delta=0.3, warmup=1, smoothing=1.0, momentum=0.9, weight_decay=4e-4)
+st = SelSyncStep(w, g, cfg, order="norm_first", tile_elems=tile, early_vote=mode == "up-early")
+if mode == "down":
+    g.mul_(1.5)
 for _ in range(5):
     st.step_async(0.01)
 st.synchronize()
+if mode in ("up", "up-early"):
+    g.mul_(1.5)
+elif mode == "down":
+    g.div_(1.5)
 cap = 8 * (P // tile + 64)
 tl = st.symm.enable_timeline(cap)
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -51,9 +65,12 @@ for name, kk in (("update", 0), ("mean", 1)):
                  np.percentile(run, 90))
 span = (ev[:, 3].max() - t0) / 1e3
 m0 = marks[0]
-lines = [f"rank {rank}: step {ms*1e3:.0f} us (events), overlapped kernel span {span:.0f} us",
-         "   vote posted {:.0f} us; first ticket {:.0f}; last arrival {:.0f}; end barrier done {:.0f} us".format(
-             (marks[1] - m0) / 1e3, (t0 - m0) / 1e3, (marks[4] - m0) / 1e3, (marks[5] - m0) / 1e3)]
+dec = st.decisions()[-1]
+lines = [f"rank {rank} [{mode}, decision {dec}]: step {ms*1e3:.0f} us (events), overlapped kernel span {span:.0f} us",
+         "   vote posted {:.0f} us; early sync posted {}; first ticket {:.0f}; last arrival {:.0f}; "
+         "end barrier done {:.0f} us".format(
+             (marks[1] - m0) / 1e3, f"{(marks[3] - m0) / 1e3:.0f} us" if marks[3] > m0 else "-", (t0 - m0) / 1e3,
+             (marks[4] - m0) / 1e3, (marks[5] - m0) / 1e3)]
 for name, (n, wt, rn, first, last, p90) in out.items():
     lines.append(f"   {name:6s} tasks {n:5d}  wait {wt:7.1f} us  run {rn:7.1f} us (p90 {p90:.1f})  "
                  f"first start {first:7.0f} us  last end {last:7.0f} us")
