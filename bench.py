@@ -77,7 +77,7 @@ def parse():
                     help="fused: the whole step in one cooperative launch (symm only)")
     ap.add_argument("--tile", type=int, default=None,
                     help="elements per tile of the overlapped sync step (default: 4096 up to 2M params, else 16384)")
-    ap.add_argument("--order", default="adaptive", choices=["update_first", "norm_first", "adaptive", "nan_safe"],
+    ap.add_argument("--order", default="auto", choices=["auto", "update_first", "norm_first", "adaptive", "nan_safe"],
                     help="one-launch step order (flag-exchange fused): norm_first overlaps update and mean")
     ap.add_argument("--early-vote", action="store_true",
                     help="norm-first orders: the exact early vote (opt-in; A/B of the mean's start)")
@@ -236,6 +236,8 @@ def reference_arm(args, rank, world):
 
 
 def workload_config(args, world):
+    from paper_2307_07950_b200.collectives import resolve_order
+
     return {
         "workload": (f"selsync hot-path step, flattened fp32 model P={args.P:,} (BASELINE configs[4] "
                      f"microbench at the north_star 100M size), SGD momentum {args.momentum} wd "
@@ -245,7 +247,8 @@ def workload_config(args, world):
         "update_kernel": "K1+K2 then K3 with 1/N pre-scale" if args.no_fuse else "fused K13+K2",
         "collective": args.collective if world > 1 else "none (single rank)",
         "flag_exchange": args.flag_exchange if world > 1 else "none (single rank)",
-        "step_order": args.order if world > 1 and args.flag_exchange == "fused" else "update_first",
+        "step_order": (resolve_order(args.order, args.P, world) if world > 1 and args.flag_exchange == "fused"
+                       else "update_first"),
         "early_vote": bool(world > 1 and args.order in ("norm_first", "adaptive") and args.early_vote),
         "decision_mix": {"sync_frac": 0.5, "grad_scales": MIX_SCALES, "smoothing": 1.0, "delta": 0.3,
                          "warmup": 1},

@@ -102,6 +102,18 @@ SIGNAL_OFFSET = 8192  # our slots sit at the top of torch's 9216-byte signal pad
 ORDERS = {"update_first": 0, "norm_first": 1, "adaptive": 2, "nan_safe": 3}
 
 
+def resolve_order(order: str, numel: int, world: int) -> str:
+    """order="auto" (the default): "adaptive" where the ticketed norm-first
+    pass pays on sync steps, else "update_first". Measured on B200 (bench
+    modes, P sweep, profiles/r02_order_size/): at N = 2 update-first is faster
+    up to 16M parameters and adaptive from 32M; at N = 4 update-first wins
+    at 4M, adaptive from 16M (the mean costs more bytes per link there, so
+    overlapping it pays earlier)."""
+    if order != "auto":
+        return order
+    return "adaptive" if numel >= (24_000_000 if world <= 2 else 10_000_000) else "update_first"
+
+
 def default_tile_elems(numel: int) -> int:
     # measured (N = 2, one graph replay per step): 4096-element tiles win
     # below ~2M parameters (more tiles than blocks), 16384 from 4M up

@@ -75,8 +75,33 @@ struct OverlapArgs {
     uint64_t* early_posted;    // early vote: seq of the last step this rank posted an early sync tag for
 };
 
-#ifndef SS_LAG_DIV
-#define SS_LAG_DIV 1
+// A/B build switches of the small-P latency study (tools/small_p_probe.py):
+// SS_VOTE_FENCE=1 restores a system fence before the vote posts. It is not
+// needed: the posts are st.release.sys, and the blocks' updates reach the
+// last block through the gpu-scope arrival counter (fence + atomic, atomic +
+// fence), and causality order is transitive across the two scopes (measured:
+// -1 to -1.5 us per step at N = 2, P = 1M-16M);
+// SS_STEP_PER_THREAD = float4 vectors per thread (per stream) below which the
+// step grid shrinks (small P: 244 instead of 592 blocks at 1M, -1.5 us per
+// local step at N = 2; one full wave from 4M up); SS_DECIDED_SLEEP = ns
+// between polls of the decision word
+#ifndef SS_VOTE_FENCE
+#define SS_VOTE_FENCE 0
+#endif
+#ifndef SS_STEP_PER_THREAD
+#define SS_STEP_PER_THREAD 4
+#endif
+#ifndef SS_DECIDED_SLEEP
+#define SS_DECIDED_SLEEP 256
+#endif
+__device__ __forceinline__ void vote_fence() {
+#if SS_VOTE_FENCE
+    __threadfence_system();
+#endif
+}
+
+#ifndef SS_LAG_SCALE
+#define SS_LAG_SCALE 1
 #endif
 
 constexpr int kEarlySync = -3;  // vote_or_early: a peer proved the step sync before its sweep ended
@@ -101,18 +126,28 @@ __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
 // (context LL -> local, SS -> sync) as well as alternations, where a single
 // EWMA would sit near 0.5 and pick the norm-first order for every local step.
 // Every rank updates it from the same agreed words: all ranks pick the same order.
-__device__ __forceinline__ float predicted_sync(const float* pr) {
-    // five independent loads, then a select: no dependent load at kernel start
+// Thread 0 of every block loads the predictor once at kernel start (five
+// independent loads, then a select: no dependent load); the last block reuses
+// that copy for the update at the end (nothing else writes the predictor
+// during a launch), so the update costs two stores and no load latency.
+struct PredCache {
+    float p[4];
+    int h;
+};
+__device__ __forceinline__ PredCache predictor_load(const float* pr) {
     const volatile float* v = pr;
-    const float p0 = v[0], p1 = v[1], p2 = v[2], p3 = v[3];
-    const int h = static_cast<int>(v[4]) & 3;
-    return h == 0 ? p0 : h == 1 ? p1 : h == 2 ? p2 : p3;
+    PredCache c;
+    c.p[0] = v[0]; c.p[1] = v[1]; c.p[2] = v[2]; c.p[3] = v[3];
+    c.h = static_cast<int>(v[4]) & 3;
+    return c;
 }
-__device__ __forceinline__ void predictor_update(float* pr, int w) {
-    const int h = static_cast<int>(pr[4]) & 3;
+__device__ __forceinline__ float pick(const PredCache& c) {
+    return c.h == 0 ? c.p[0] : c.h == 1 ? c.p[1] : c.h == 2 ? c.p[2] : c.p[3];
+}
+__device__ __forceinline__ void predictor_update(float* pr, const PredCache& c, int w) {
     const int s = w == SS_FLAG_SYNC ? 1 : 0;
-    pr[h] = 0.75f * pr[h] + (s ? 0.25f : 0.0f);
-    pr[4] = static_cast<float>(((h << 1) | s) & 3);
+    pr[c.h] = 0.75f * pick(c) + (s ? 0.25f : 0.0f);
+    pr[4] = static_cast<float>(((c.h << 1) | s) & 3);
 }
 
 // bounded spin until *p >= want (gpu scope); sets the error word on timeout
@@ -215,7 +250,7 @@ __device__ void known_tile_done(const Finish& f, const SymmArgs& s, const Overla
         wait_count_gpu(o.started, static_cast<unsigned int>(vb.n), s);
         signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
         const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
-        __threadfence_system();
+        vote_fence();
         for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
     }
@@ -236,12 +271,13 @@ __device__ __forceinline__ bool sync_known_ahead(const Finish& f) {
 // only a known snapshot counts itself in `started` (no 1-per-block atomic on
 // other steps): K2 of the known pass waits for all of them, hence every block
 // reads the state before K2 changes it and takes the known snapshot too.
-__device__ int order_snapshot(const Finish& f, const OverlapArgs& o) {
+// pc: thread 0's copy of the predictor (adaptive mode), for the update at the end.
+__device__ int order_snapshot(const Finish& f, const OverlapArgs& o, PredCache* pc) {
     __shared__ int s_order;
     if (threadIdx.x == 0) {
+        if (o.mode == 2) *pc = predictor_load(o.predictor);
         const bool known = (o.mode == 1 || o.mode == 2) && o.tile_norm != nullptr && sync_known_ahead(f);
-        const bool nf = known || o.mode == 1 || o.mode == 3 ||
-                        (o.mode == 2 && predicted_sync(o.predictor) >= o.threshold);
+        const bool nf = known || o.mode == 1 || o.mode == 3 || (o.mode == 2 && pick(*pc) >= o.threshold);
         s_order = (nf ? kNormFirst : 0) | (known ? kKnown : 0) | (o.mode == 3 ? kSafe : 0);
         if (known) {
             __threadfence();  // the state reads above complete before the arrival below
@@ -254,7 +290,7 @@ __device__ int order_snapshot(const Finish& f, const OverlapArgs& o) {
 
 template <bool MOM, bool NEST, int W>
 __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
-                                     uint64_t seq, bool known, bool safe, VBlk vb) {
+                                     uint64_t seq, bool known, bool safe, VBlk vb, const PredCache& pc) {
     __shared__ unsigned long long s_ticket;
     __shared__ int s_vote;
     __shared__ bool s_last;
@@ -325,7 +361,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                 if (early) *o.running = 0.0;  // every block has added its partial
                 signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
                 const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
-                __threadfence_system();
+                vote_fence();
                 for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
                 if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
             }
@@ -442,7 +478,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
         if (o.dbg) o.dbg[4 * o.dbg_cap + 4] = now_ns();
         *f.word = w;
         if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
-        if (o.mode == 2) predictor_update(o.predictor, w);
+        if (o.mode == 2) predictor_update(o.predictor, pc, w);
         // known: the mean ran in any case; early: it may have run on an error step
         if (w == SS_FLAG_SYNC || known || (early && w > 0)) end_barrier(s, seq);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 5] = now_ns();
@@ -462,7 +498,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
 // no second launch, no device-side launch.
 template <bool MOM, bool NEST, int W>
 __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const SymmArgs& s, const OverlapArgs& o,
-                                     uint64_t seq, VBlk vb) {
+                                     uint64_t seq, VBlk vb, const PredCache& pc) {
     __shared__ bool s_last;
     __shared__ int s_w;
     uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;
@@ -472,9 +508,9 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
     const double bsum = block_sum(acc);
     if (threadIdx.x == 0) {
         ws.partials[vb.bid] = bsum;
-        // gpu scope suffices: the last block observes this counter and issues
-        // the system-scope fence before its release of the vote (causality is
-        // transitive), so peers reading after the vote see these stores
+        // gpu scope suffices: the last block observes this counter, then
+        // releases the vote at system scope (causality is transitive), so
+        // peers reading after the vote see these stores
         __threadfence();
         s_last = atomicAdd(ws.counter, 1u) == static_cast<unsigned int>(vb.n - 1);
     }
@@ -488,20 +524,20 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
             *ws.counter = 0u;
             signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
             const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
-            __threadfence_system();
+            vote_fence();
             for (int j = 0; j < s.world; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
             if (mark) mark[1] = now_ns();
             const int w = agreed_vote(s, seq);
             if (mark) mark[2] = now_ns();
             *f.word = w;
             if (s.agreed_ring && s.ring_cap > 0) s.agreed_ring[(seq - 1) % s.ring_cap] = w;
-            if (o.mode == 2) predictor_update(o.predictor, w);
-            st_release_gpu(decided, (seq << 32) | static_cast<uint32_t>(w));
+            st_release_gpu(decided, (seq << 32) | static_cast<uint32_t>(w));  // the waiting blocks first
             s_w = w;
+            if (o.mode == 2) predictor_update(o.predictor, pc, w);
         }
     } else if (threadIdx.x == 0) {
         bool to = false;
-        const uint64_t t = wait_tag_gpu(decided, seq, s.timeout_ns, &to);
+        const uint64_t t = wait_tag_gpu(decided, seq, s.timeout_ns, &to, SS_DECIDED_SLEEP);
         if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
         s_w = to ? -1 : static_cast<int>(static_cast<uint32_t>(t));
     }
@@ -525,14 +561,15 @@ __device__ __forceinline__ void step_body(const SgdArgs& a, const Finish& f, con
                                           VBlk vb) {
     const uint64_t seq = static_cast<uint64_t>(*reinterpret_cast<volatile uint32_t*>(s.seq)) + 1;
     // the order of this step: identical on every rank (same decision history)
-    const int order = order_snapshot(f, o);
+    PredCache pc{};
+    const int order = order_snapshot(f, o, &pc);
     uint64_t* mark = o.dbg ? o.dbg + 4 * o.dbg_cap : nullptr;  // {start, vote posted, votes in, -, last arrival, end}
     if (mark && vb.bid == 0 && threadIdx.x == 0) mark[0] = now_ns();
     if (order & kNormFirst) {
-        nf_body<MOM, NEST, W>(a, f, s, o, seq, (order & kKnown) != 0, (order & kSafe) != 0, vb);
+        nf_body<MOM, NEST, W>(a, f, s, o, seq, (order & kKnown) != 0, (order & kSafe) != 0, vb, pc);
         return;
     }
-    uf_body<MOM, NEST, W>(a, f, s, o, seq, vb);
+    uf_body<MOM, NEST, W>(a, f, s, o, seq, vb, pc);
 }
 
 template <bool MOM, bool NEST, int W>
@@ -582,7 +619,7 @@ __device__ __forceinline__ void ga_body(const SgdArgs& a, const Finish& f, const
                 *ws.counter = 0u;
                 signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
                 const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
-                __threadfence_system();
+                vote_fence();
                 for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
             }
         }
@@ -715,12 +752,12 @@ template <bool MOM, bool NEST, int W>
 int launch_step(const SgdArgs& a, Finish f, const SymmArgs& sa, OverlapArgs o, int max_blocks, void* stream) {
     static int res_step = 0;
     if (res_step == 0) res_step = occupancy(step_kernel<MOM, NEST, W>, kThreads);
-    const int grid = step_grid((a.n - a.head) / 4 + 1, MOM ? 1 : 2, res_step, max_blocks);
+    const int grid = step_grid((a.n - a.head) / 4 + 1, (MOM ? 1 : 2) * SS_STEP_PER_THREAD, res_step, max_blocks);
     f.total_blocks = grid;
     // norm-first pass: the in-flight window is ~grid tickets = grid / (N + 1)
     // groups; the mean of a tile is scheduled one window after its update
-    // (SS_LAG_DIV: A/B builds of a shorter lag)
-    o.lag = grid / (sa.world + 1) / SS_LAG_DIV + 2;
+    // (SS_LAG_SCALE: A/B builds of another lag; 1/2, 1/4 and 0 measured slower)
+    o.lag = static_cast<int>(grid / (sa.world + 1) * SS_LAG_SCALE) + 2;
     return launch_coop(step_kernel<MOM, NEST, W>, grid, stream, "ss_step_symm_f32", a, f, sa, o);
 }
 

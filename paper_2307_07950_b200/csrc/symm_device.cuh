@@ -122,7 +122,8 @@ __device__ __forceinline__ uint64_t ld_relaxed_gpu(const uint64_t* p) {
 // value. Up to a few hundred blocks poll one word while the slowest blocks
 // still stream: relaxed polls with a back-off keep that traffic light, one
 // acquire fence after the match orders what follows.
-__device__ uint64_t wait_tag_gpu(const uint64_t* p, uint64_t want, uint64_t timeout_ns, bool* timed_out) {
+__device__ uint64_t wait_tag_gpu(const uint64_t* p, uint64_t want, uint64_t timeout_ns, bool* timed_out,
+                                 unsigned sleep_ns = 256) {
     const uint64_t t0 = now_ns();
     uint64_t v = ld_relaxed_gpu(p);
     while ((v >> 32) != want) {
@@ -130,7 +131,7 @@ __device__ uint64_t wait_tag_gpu(const uint64_t* p, uint64_t want, uint64_t time
             *timed_out = true;
             return v;
         }
-        __nanosleep(256);
+        __nanosleep(sleep_ns);
         v = ld_relaxed_gpu(p);
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");

@@ -62,7 +62,7 @@ from typing import Optional
 import torch
 
 from . import kernels as K
-from .collectives import RankGroup
+from .collectives import RankGroup, resolve_order
 from .config import SelSyncConfig
 from .errors import ConfigError
 
@@ -83,7 +83,7 @@ class SelSyncStep:
         broadcast_init: bool = True,
         profile: bool = False,
         timeout_s: float = 10.0,
-        order: str = "adaptive",
+        order: str = "auto",
         order_threshold: float = 0.2,
         tile_elems: Optional[int] = None,
         multicast="auto",
@@ -124,6 +124,8 @@ class SelSyncStep:
         self.collective = collective if (self.world > 1 or collective == "symm"
                                         and (colocated or torch.distributed.is_initialized())) else "none"
         self.flag_exchange = flag_exchange
+        # "auto": adaptive where the overlapped norm-first pass pays, else update-first
+        order = resolve_order(order, params.numel(), self.world)
         # NaN-safe: a step on which any rank observes a NaN norm changes no
         # rank's parameters (the reference raises in observe, signal.py:67-68,
         # before sgd_step, strategies.py:286 vs :383). The fused update + norm

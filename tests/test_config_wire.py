@@ -75,3 +75,17 @@ def test_integration_doc_names_resolve():
                  "FlatParameters", "SelSyncStep", "LrSchedule", "lr_at", "SelSyncTrainer",
                  "TensorListSelSyncStep", "ReplicaSelSync", "RankGroup"):
         assert getattr(S, name) is not None, name
+
+
+def test_auto_order_picks_update_first_for_small_models():
+    """order="auto" (the SelSyncStep default): the overlapped norm-first pass
+    only where it was measured faster on sync steps (profiles/r02_order_size)."""
+    from paper_2307_07950_b200.collectives import resolve_order
+
+    assert resolve_order("auto", 16_000_000, 2) == "update_first"
+    assert resolve_order("auto", 32_000_000, 2) == "adaptive"
+    assert resolve_order("auto", 4_000_000, 4) == "update_first"
+    assert resolve_order("auto", 16_000_000, 4) == "adaptive"
+    assert resolve_order("auto", 100_000_000, 8) == "adaptive"
+    for o in ("update_first", "norm_first", "adaptive", "nan_safe"):
+        assert resolve_order(o, 1000, 2) == o

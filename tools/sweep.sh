@@ -1,11 +1,13 @@
 #!/bin/bash
 # BASELINE configs[4]: flattened parameter sweep 1M-1B, forced all-local / all-sync
 # and the 50% mix, at N in $NS (default "1 2 4"). P <= 16M replays one CUDA graph
-# per step (launch-bound sizes); larger P uses the host launch path with events.
+# per step at N = 1 (launch-bound sizes); everything else uses the host launch path.
 NS=${NS:-"1 2 4"}
 SIZES=${SIZES:-"1000000 4000000 16000000 64000000 100000000 256000000 1000000000"}
 mkdir -p gpurun_out/sweep
 for P in $SIZES; do
+  # graph replay only at N = 1: at N > 1 eager cooperative launches measured faster
+  # (profiles/r02_small_p/max_blocks_n2.txt)
   G=""; [ "$P" -le 16000000 ] && G="--graph"
   for N in $NS; do
     if [ "$N" = "1" ]; then
@@ -13,7 +15,7 @@ for P in $SIZES; do
         > gpurun_out/sweep/n1_$P.json 2> gpurun_out/sweep/n1_$P.err
     else
       timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
-        --master-port 2952$N bench.py --gpus $N --P $P --steps 50 --warmup 5 --no-e2e $G \
+        --master-port 2952$N bench.py --gpus $N --P $P --steps 50 --warmup 5 --no-e2e --no-replay \
         > gpurun_out/sweep/n${N}_$P.json 2> gpurun_out/sweep/n${N}_$P.err
     fi
   done
