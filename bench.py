@@ -81,6 +81,9 @@ def parse():
                     help="one-launch step order (flag-exchange fused): norm_first overlaps update and mean")
     ap.add_argument("--early-vote", action="store_true",
                     help="norm-first orders: the exact early vote (opt-in; A/B of the mean's start)")
+    ap.add_argument("--no-kernel-events", action="store_true",
+                    help="no per-launch CUDA events (latency-bound small P: the events themselves cost "
+                         "a few us per step); the roofline then uses the whole local step time")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-replay", action="store_true", help="skip the replayed golden decision patterns")
@@ -283,7 +286,7 @@ def main():
 
     from paper_2307_07950_b200 import SelSyncConfig
     from paper_2307_07950_b200 import kernels as K
-    from paper_2307_07950_b200.collectives import RankGroup
+    from paper_2307_07950_b200.collectives import RankGroup, resolve_order
     from paper_2307_07950_b200.step import SelSyncStep
 
     torch.cuda.set_device(local)
@@ -311,7 +314,7 @@ def main():
         st = SelSyncStep(w, g, cfg, momentum_buffer=mom, group=comm, fuse=not args.no_fuse,
                          collective=args.collective if world > 1 else None,
                          flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
-                         trace_capacity=1 << 14, profile=not args.graph, order=args.order, tile_elems=args.tile,
+                         trace_capacity=1 << 14, profile=not (args.graph or args.no_kernel_events), order=args.order, tile_elems=args.tile,
                          early_vote=args.early_vote)
         return st
 
@@ -456,14 +459,16 @@ def main():
     # N > 1 with the one-launch step this also holds the vote exchange)
     kms = sorted(modes["all_local"]["kernel_ms"])
     timed_on = "all_local mode, CUDA events around every launch on the launching stream"
-    if not kms:  # --graph: no events inside graphs; bound the kernel by the whole local step
+    if not kms:  # --graph / --no-kernel-events: bound the kernel by the whole local step
         kms = [modes["all_local"]["ms"] / args.steps]
-        timed_on = "all_local step time under graph replay (upper bound of the kernel time)"
+        timed_on = ("all_local step time under graph replay (upper bound of the kernel time)" if args.graph else
+                    "all_local step time without per-launch events (upper bound of the kernel time)")
     k_mean = sum(kms) / len(kms)
     bytes_per_launch = (20 if args.momentum else 12) * P
     if args.no_fuse:
         bytes_per_launch = 4 * P
-    if one_launch and args.order == "norm_first":
+    order_eff = resolve_order(args.order, P, world)
+    if one_launch and order_eff == "norm_first":
         bytes_per_launch += 4 * P  # norm pass first, then the plain update (both inside the launch)
     achieved = bytes_per_launch / (k_mean * 1e-3) / 1e9
     kernel_name = ("ss_update_norm_signal_f32 (K13+K2: fused SGD-momentum-wd update + ||g||^2 + signal step)"
@@ -473,7 +478,7 @@ def main():
         kernel_name = ("ss_step_symm_f32 (one cooperative launch: K13+K2, the P2P vote exchange in the last "
                        "block, and on sync steps the NVLink mean by every block of the same grid; timed on "
                        "local steps)")
-        traffic_key = f"step_kernel_w{world}"
+        traffic_key = "step_kernel_local"  # update-first local step; ncu runs single-GPU commands only
     sync_frac = sum(1 for d in res["decisions"] if d) / len(res["decisions"])
     line = {
         "metric": METRIC,
@@ -499,6 +504,7 @@ def main():
             "unit": "GB/s",
             "frac": achieved / hbm_peak,
             "traffic": traffic_from_profiles(traffic_key, P),
+            "traffic_source": traffic_from_profiles(traffic_key, P, field="source"),
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "kernel_ms_mean": k_mean,
             "kernel_ms_median": kms[len(kms) // 2],
@@ -514,7 +520,7 @@ def main():
                "kernel_ms_mean": sum(m["kernel_ms"]) / len(m["kernel_ms"]) if m["kernel_ms"] else None}
         ent.update(exchange_stats(m, P, world))
         ent["delta"] = 1e9 if name == "all_local" else 0.0
-        if name == "all_sync" and one_launch and args.order != "update_first":
+        if name == "all_sync" and one_launch and order_eff != "update_first":
             ent["note"] = ("delta = 0: every step is sync before ||g||^2 is known, so the one-launch step "
                            "takes the known-sync pass (no norm sweep, mean overlapped from the first tile)")
         line["modes"][name] = ent
@@ -702,16 +708,18 @@ def exchange_stats(m, P, world):
     return out
 
 
-def traffic_from_profiles(kernel, P):
+def traffic_from_profiles(kernel, P, field="dram_bytes_per_launch"):
     """dram read+write bytes per launch of THIS roofline kernel (sgd_kernel =
-    K13, step_kernel_w<N> = the one-launch step at N ranks, local step) from
-    the committed ncu --set full summaries at the same P, if one exists."""
+    K13; step_kernel_local = the one-launch step kernel's update-first local
+    step, captured through a world-1 group because ncu only profiles
+    single-GPU commands) from the committed ncu --set full summaries at the
+    same P, if one exists; field="source" names the capture."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
     try:
         ent = json.loads(p.read_text()).get(kernel, {}).get(str(P))
-        return None if ent is None else ent["dram_bytes_per_launch"]
+        return None if ent is None else ent[field]
     except Exception:
         return None
 

@@ -9,13 +9,15 @@ for P in $SIZES; do
   # graph replay only at N = 1: at N > 1 eager cooperative launches measured faster
   # (profiles/r02_small_p/max_blocks_n2.txt)
   G=""; [ "$P" -le 16000000 ] && G="--graph"
+  # and at N > 1 without per-launch events there (they cost a few us per step)
+  E=""; [ "$P" -le 16000000 ] && E="--no-kernel-events"
   for N in $NS; do
     if [ "$N" = "1" ]; then
       timeout 600 python bench.py --P $P --steps 50 --warmup 5 --no-e2e --no-cpu-baseline $G \
         > gpurun_out/sweep/n1_$P.json 2> gpurun_out/sweep/n1_$P.err
     else
       timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
-        --master-port 2952$N bench.py --gpus $N --P $P --steps 50 --warmup 5 --no-e2e --no-replay \
+        --master-port 2952$N bench.py --gpus $N --P $P --steps 50 --warmup 5 --no-e2e --no-replay $E \
         > gpurun_out/sweep/n${N}_$P.json 2> gpurun_out/sweep/n${N}_$P.err
     fi
   done
