@@ -60,6 +60,8 @@ int check_launch(const char* what) {
 template <int U>
 __global__ void __launch_bounds__(kThreads, 4) norm_kernel(const float* __restrict__ g, int64_t n,
                                                         int64_t head, Finish f) {
+    pdl_wait();
+    pdl_trigger();
     finish_norm(f, norm_pass<U>(g, n, head));
 }
 
@@ -72,6 +74,8 @@ __global__ void signal_kernel(ss_signal_state* st, const double* x, double delta
 
 template <bool MOM, bool NEST, bool NORM, int U, int CP = 0>
 __global__ void __launch_bounds__(kThreads, 4) sgd_kernel(SgdArgs a, Finish f) {
+    pdl_wait();
+    pdl_trigger();
     const double acc = sgd_pass<MOM, NEST, NORM, U, CP>(a);
     if (NORM) finish_norm(f, acc);
 }
@@ -187,7 +191,7 @@ int launch_norm_u(const float* g, int64_t n, Finish f, void* stream, const char*
     const int64_t head = n ? common_head(n, g, nullptr, nullptr) : 0;
     const int grid = static_cast<int>(grid_for((n - head) / 4 + 1, U, resident));
     f.total_blocks = grid;
-    norm_kernel<U><<<grid, kThreads, 0, as_stream(stream)>>>(g, n, head, f);
+    (void)launch_ex(norm_kernel<U>, grid, kThreads, as_stream(stream), false, g, n, head, f);
     return check_launch(what);
 }
 
@@ -397,7 +401,7 @@ int launch_sgd_v(const SgdArgs& a, const Finish& f0, void* stream) {
     const int grid = static_cast<int>(grid_for((a.n - a.head) / 4 + 1, U, resident));
     Finish f = f0;
     f.total_blocks = grid;
-    sgd_kernel<MOM, NEST, NORM, U, CP><<<grid, kThreads, 0, as_stream(stream)>>>(a, f);
+    (void)launch_ex(sgd_kernel<MOM, NEST, NORM, U, CP>, grid, kThreads, as_stream(stream), false, a, f);
     return check_launch(NORM ? "ss_update_norm_signal_f32" : "ss_sgd_update_f32");
 }
 

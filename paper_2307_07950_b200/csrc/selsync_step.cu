@@ -574,6 +574,8 @@ __device__ __forceinline__ void step_body(const SgdArgs& a, const Finish& f, con
 
 template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
+    pdl_wait();
+    pdl_trigger();
     step_body<MOM, NEST, W>(a, f, s, o, hw_blk());
 }
 
@@ -693,6 +695,8 @@ __device__ __forceinline__ void ga_body(const SgdArgs& a, const Finish& f, const
 
 template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel(SgdArgs a, Finish f, SymmArgs s, OverlapArgs o) {
+    pdl_wait();
+    pdl_trigger();
     ga_body<MOM, NEST, W>(a, f, s, o, hw_blk());
 }
 
@@ -728,17 +732,7 @@ int step_grid(int64_t vec_work, int per_thread, int resident, int max_blocks) {
 // letting a partly placed grid spin into the timeout. Capturable in CUDA graphs.
 template <typename... P, typename... A>
 int launch_coop(void (*kernel)(P...), int grid, void* stream, const char* what, A... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = static_cast<cudaStream_t>(stream);
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = coop_enabled() ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+    const cudaError_t e = launch_ex(kernel, grid, kThreads, static_cast<cudaStream_t>(stream), coop_enabled(), args...);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
         return fail(e == cudaErrorCooperativeLaunchTooLarge ? SS_ERR_CONFIG : SS_ERR_CUDA,
@@ -895,6 +889,8 @@ __device__ __forceinline__ const RankArgs& load_rank_args(const RankArgs* __rest
 template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_kernel_colo(const RankArgs* __restrict__ args, int per_rank,
                                                                 float lr, int first) {
+    pdl_wait();
+    pdl_trigger();
     const int rank = static_cast<int>(blockIdx.x) / per_rank;
     const RankArgs& ra = load_rank_args(args, rank, lr, first);
     step_body<MOM, NEST, W>(ra.a, ra.f, ra.s, ra.o, VBlk{static_cast<int>(blockIdx.x) % per_rank, per_rank});
@@ -903,6 +899,8 @@ __global__ void __launch_bounds__(kThreads, 4) step_kernel_colo(const RankArgs* 
 template <bool MOM, bool NEST, int W>
 __global__ void __launch_bounds__(kThreads, 4) step_ga_kernel_colo(const RankArgs* __restrict__ args, int per_rank,
                                                                    float lr, int first) {
+    pdl_wait();
+    pdl_trigger();
     const int rank = static_cast<int>(blockIdx.x) / per_rank;
     const RankArgs& ra = load_rank_args(args, rank, lr, first);
     ga_body<MOM, NEST, W>(ra.a, ra.f, ra.s, ra.o, VBlk{static_cast<int>(blockIdx.x) % per_rank, per_rank});
@@ -1050,11 +1048,13 @@ extern "C" int ss_colocated_step_f32(const ss_colocated_plan* plan, float lr, in
     cfg.gridDim = dim3(static_cast<unsigned>(plan->ranks * per_rank));
     cfg.blockDim = dim3(kThreads);
     cfg.stream = static_cast<cudaStream_t>(stream);
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     const cudaError_t e = cudaLaunchKernelExC(&cfg, kern, params);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
