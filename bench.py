@@ -65,7 +65,10 @@ def parse():
     ap.add_argument("--delta", type=float, default=0.3, help="delta for model workloads")
     ap.add_argument("--graph", action="store_true",
                     help="model workloads: capture fwd + bwd + SelSync step in one CUDA graph; microbench: "
-                         "replay one captured step per gradient buffer (launch-bound small P)")
+                         "replay captured steps (launch-bound small P)")
+    ap.add_argument("--graph-steps", type=int, default=4,
+                    help="microbench --graph: consecutive steps per captured graph (the gradient ring in order; "
+                         "remainders replay one-step graphs)")
     ap.add_argument("--sel-warmup", type=int, default=25, help="EWMA window / warmup for model workloads")
     ap.add_argument("--momentum", type=float, default=0.9)
     ap.add_argument("--weight-decay", type=float, default=4e-4)
@@ -263,8 +266,10 @@ def workload_config(args, world):
                if 12 * args.P > 126e6 else
                f"inputs fit in L2 ({12 * args.P / 1e6:.1f} MB, not flushed): a small-P sweep point, "
                "launch/latency-bound, not a bandwidth claim"),
-        "launch": ("one CUDA graph replay per step (captured per gradient buffer)" if args.graph
-                   else "one host launch per step"),
+        "launch": ((f"CUDA graphs of {args.graph_steps} consecutive steps (the gradient ring in order, "
+                    "programmatic dependent launch between the step kernels inside a graph)"
+                    if args.graph_steps > 1 else "one CUDA graph replay per step (captured per gradient buffer)")
+                   if args.graph else "one host launch per step (programmatic dependent launch)"),
     }
 
 
@@ -350,8 +355,19 @@ def main():
                 host_row.copy_(step.signal.trace[32 * r:32 * r + 32], non_blocking=True)
                 cur.synchronize()
             return
-        for _ in range(n):
+        i = 0
+        while i < n:
+            i += 1
             k = step.steps_done % 4 if schedule is None else schedule[step.steps_done % len(schedule)]
+            G = args.graph_steps
+            if (args.graph and step.async_capable and step.steps_done > 0 and schedule is None and host_ring is None
+                    and G > 1 and n - i + 1 >= G):
+                graphs = captured.setdefault(id(step), {})
+                if ("multi", k) not in graphs:
+                    graphs[("multi", k)] = step.capture(args.lr, [grads_ring[(k + j) % 4] for j in range(G)])
+                graphs[("multi", k)].replay()
+                i += G - 1
+                continue
             if host_ring is not None:
                 step.grads = g
                 g.copy_(host_ring[k], non_blocking=True)

@@ -368,6 +368,27 @@ SS_API int ss_colocated_prepare_f32(const ss_rank_step* ranks_host, int32_t rank
                                     int32_t max_blocks_per_rank, ss_colocated_plan* plan_host, void* stream);
 SS_API int ss_colocated_step_f32(const ss_colocated_plan* plan_host, float lr, int32_t first_step, void* stream);
 
+/* ---------------- prepared per-rank step (the lean per-step host path) ---------------- */
+
+/* One rank's step with everything but the gradient pointer, lr and the
+   first-step flag validated once. init checks what the per-call entry points
+   check on every call -- group == NULL: one rank, ss_update_norm_signal_f32
+   (K13+K2); otherwise ss_step_symm_f32, or ss_step_symm_ga_f32 when grads = 1
+   -- picks the kernel and keeps its argument blocks in the caller's plan;
+   launch patches g_dev, lr and first_step and issues the same launch
+   (cooperative for the group kernels; CUDA-graph capturable). The group is
+   read at init: re-init after changing it. This is the per-step call of
+   _selsync_step (strategies.py:369-403) made as one 5-argument C call: a
+   step of a small model is shorter than marshalling the 18 arguments of the
+   per-call entry points (1M parameters: ~8 us of GPU work per step). */
+#define SS_STEP_PLAN_WORDS 192
+typedef struct ss_step_plan {
+    uint64_t opaque[SS_STEP_PLAN_WORDS];
+} ss_step_plan;
+SS_API int ss_step_plan_init(ss_step_plan* plan_host, const ss_rank_step* rank_host, int32_t grads);
+SS_API int ss_step_plan_launch(const ss_step_plan* plan_host, const float* g_dev, float lr, int32_t first_step,
+                               void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,7 +96,8 @@ class SymmGroupC(Structure):
 
 
 class RankStepC(Structure):
-    """ss_rank_step -- one colocated rank's step arguments (pointers + hyperparameters)."""
+    """ss_rank_step -- one rank's step arguments (pointers + hyperparameters): a
+    colocated rank's, or the input of ss_step_plan_init."""
 
     _fields_ = [
         ("w", c_void_p), ("g", c_void_p), ("m", c_void_p), ("n", c_int64),
@@ -111,6 +112,15 @@ class ColocatedPlanC(Structure):
 
     _fields_ = [("args_dev", c_void_p), ("ranks", c_int32), ("blocks_per_rank", c_int32), ("grads", c_int32),
                 ("flags", c_int32)]
+
+
+STEP_PLAN_WORDS = 192  # SS_STEP_PLAN_WORDS
+
+
+class StepPlanC(Structure):
+    """ss_step_plan -- opaque storage of a prepared per-rank step."""
+
+    _fields_ = [("opaque", ctypes.c_uint64 * STEP_PLAN_WORDS)]
 
 
 _P = c_void_p
@@ -170,6 +180,8 @@ _SIGS = {
     "ss_colocated_args_bytes": ([c_int32, POINTER(c_int64)], c_int),
     "ss_colocated_prepare_f32": ([c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p], c_int),
     "ss_colocated_step_f32": ([c_void_p, c_float, c_int32, c_void_p], c_int),
+    "ss_step_plan_init": ([c_void_p, c_void_p, c_int32], c_int),
+    "ss_step_plan_launch": ([c_void_p, c_void_p, c_float, c_int32, c_void_p], c_int),
     "ss_step_symm_f32": (
         [_P, _P, _P, c_int64, c_float, c_float, c_float, c_float, c_int32, c_int32,
          _P, c_double, _P, _P, c_int32, POINTER(SymmGroupC), _P, _P],

@@ -185,6 +185,7 @@ class SymmetricView:
         g.n_tiles = int(self.n_tiles)
         self.group_c = g
         self.group_ref = ctypes.byref(g)
+        self.version = 0  # bumped on every change of group_c (prepared step plans read it once)
 
     def set_early_vote(self, on: bool) -> None:
         """Exact early vote of the norm-first orders (opt-in): the
@@ -192,6 +193,7 @@ class SymmetricView:
         from . import _native as N
 
         self.group_c.order_mode = ORDERS[self.order] | (N.ORDER_EARLY_VOTE if on else 0)
+        self.version += 1
 
     def sync_(self, word: torch.Tensor, ws_ptr: int, *, exchange: bool, stream: int) -> None:
         from . import _native as N
@@ -206,6 +208,7 @@ class SymmetricView:
         self.timeline = torch.zeros(4 * int(capacity) + 8, dtype=torch.int64, device=self.device)
         self.group_c.debug_events = self.timeline.data_ptr()
         self.group_c.debug_cap = int(capacity)
+        self.version += 1
         return self.timeline
 
     @property

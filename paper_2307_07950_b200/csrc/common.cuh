@@ -15,6 +15,9 @@ int fail(int code, const char* fmt, ...);
 int check_launch(const char* what);
 // multiprocessor count of the current device
 int sm_count();
+// K13+K2 kernel (fused update + ||g||^2 + signal step) for a prepared step,
+// and the float4 vectors per thread and stream its grid is sized for
+void* k13_kernel(bool mom, bool nest, int* per_thread);
 
 }  // namespace ss_internal
 
@@ -76,6 +79,31 @@ cudaError_t launch_ex(void (*kernel)(P...), int grid, int threads, cudaStream_t 
     cfg.attrs = attr;
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// the same through an untyped kernel entry and an argument pointer array
+inline cudaError_t launch_ex_c(const void* kernel, int grid, int threads, cudaStream_t stream, bool coop,
+                               void** params) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (coop) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelExC(&cfg, kernel, params);
 }
 
 }  // namespace

@@ -425,6 +425,12 @@ int dispatch_sgd(const SgdArgs& a, const Finish& f, bool mom, bool nest, void* s
 }
 
 
+
+template <bool MOM, bool NEST>
+void* k13_kernel_ptr() {
+    return reinterpret_cast<void*>(sgd_kernel<MOM, NEST, true, kSgdUnroll<MOM>, 0>);
+}
+
 }  // namespace
 
 extern "C" {
@@ -522,3 +528,12 @@ int ss_replica_flag_max_i32(int32_t* const* words, int32_t count, void* stream) 
 }
 
 }  // extern "C"
+
+namespace ss_internal {
+// the K13+K2 kernel of a prepared step (ss_step_plan_init) and its grid factor
+void* k13_kernel(bool mom, bool nest, int* per_thread) {
+    *per_thread = mom ? kSgdUnroll<true> : kSgdUnroll<false>;
+    if (!mom) return k13_kernel_ptr<false, false>();
+    return nest ? k13_kernel_ptr<true, true>() : k13_kernel_ptr<true, false>();
+}
+}  // namespace ss_internal

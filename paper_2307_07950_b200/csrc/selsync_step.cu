@@ -50,6 +50,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 using ss_internal::check_launch;
 using ss_internal::fail;
@@ -1062,4 +1063,129 @@ extern "C" int ss_colocated_step_f32(const ss_colocated_plan* plan, float lr, in
                     "ss_colocated_step_f32: %s (%d ranks x %d blocks)", cudaGetErrorString(e), plan->ranks, per_rank);
     }
     return check_launch("ss_colocated_step_f32");
+}
+
+// ------------------------------------------------ prepared per-rank step
+//
+// ss_step_plan_init validates a rank's step once (what ss_update_norm_signal_f32
+// / ss_step_symm_f32 / ss_step_symm_ga_f32 check on every call), picks the
+// kernel and keeps the argument blocks; ss_step_plan_launch patches the
+// gradient, lr and first-step flag and launches. At small P the per-step host
+// path is the step's cost, so the launch is one short call.
+
+namespace {
+
+constexpr uint32_t kPlanMagic = 0x53535031u;  // "SSP1"
+
+struct PlanImpl {
+    uint32_t magic;
+    int32_t kind;        // 0: K13+K2 (one rank, no group), 1: one-launch step, 2: its GA form
+    int32_t resident;    // blocks per SM of the kernel
+    int32_t per_thread;  // float4 vectors per thread and stream the grid is sized for
+    int32_t max_blocks;
+    int32_t world;
+    void* kernel;
+    RankArgs r;
+};
+static_assert(sizeof(PlanImpl) <= sizeof(ss_step_plan), "ss_step_plan too small for the argument blocks");
+
+template <bool MOM, bool NEST>
+void* step_kernel_for_width(int width, bool ga) {
+    switch (width) {
+        case 0: return ga ? reinterpret_cast<void*>(step_ga_kernel<MOM, NEST, 0>) : reinterpret_cast<void*>(step_kernel<MOM, NEST, 0>);
+        case 1: return ga ? reinterpret_cast<void*>(step_ga_kernel<MOM, NEST, 1>) : reinterpret_cast<void*>(step_kernel<MOM, NEST, 1>);
+        case 2: return ga ? reinterpret_cast<void*>(step_ga_kernel<MOM, NEST, 2>) : reinterpret_cast<void*>(step_kernel<MOM, NEST, 2>);
+        case 4: return ga ? reinterpret_cast<void*>(step_ga_kernel<MOM, NEST, 4>) : reinterpret_cast<void*>(step_kernel<MOM, NEST, 4>);
+        case 8: return ga ? reinterpret_cast<void*>(step_ga_kernel<MOM, NEST, 8>) : reinterpret_cast<void*>(step_kernel<MOM, NEST, 8>);
+        default: return nullptr;
+    }
+}
+
+void* step_kernel_any(int width, bool ga, bool mom, bool nest) {
+    if (!mom) return step_kernel_for_width<false, false>(width, ga);
+    return nest ? step_kernel_for_width<true, true>(width, ga) : step_kernel_for_width<true, false>(width, ga);
+}
+
+}  // namespace
+
+extern "C" int ss_step_plan_init(ss_step_plan* plan, const ss_rank_step* x, int32_t grads) {
+    if (!plan || !x) return fail(SS_ERR_CONFIG, "null plan or rank descriptor");
+    std::memset(plan, 0, sizeof(*plan));
+    PlanImpl p{};
+    const bool ga = grads != 0, mom = x->momentum != 0.0f, nest = x->nesterov != 0;
+    int rc;
+    if (!x->group) {
+        // one rank without a group: K13+K2 (ss_update_norm_signal_f32)
+        if (ga) return fail(SS_ERR_CONFIG, "gradient aggregation needs a symmetric group");
+        rc = make_sgd_args(&p.r.a, x->w_dev, x->g_dev, x->m_dev, x->n, 0.0f, x->momentum, x->dampening,
+                           x->weight_decay, x->nesterov, 0, nullptr, 1.0f);
+        if (rc) return rc;
+        if (!x->st_dev || !x->ws_dev) return fail(SS_ERR_CONFIG, "null state/workspace");
+        rc = check_delta_impl(x->delta);
+        if (rc) return rc;
+        rc = check_trace(x->trace_dev, x->trace_cap);
+        if (rc) return rc;
+        p.r.f = Finish{x->ws_dev, 0, 0, nullptr, x->st_dev, x->delta, x->word_dev, x->trace_dev, x->trace_cap};
+        p.kind = 0;
+        p.kernel = ss_internal::k13_kernel(mom, nest, &p.per_thread);
+        p.world = 1;
+    } else {
+        rc = build_rank_args(ga, x->w_dev, x->g_dev, x->m_dev, x->n, 0.0f, x->momentum, x->dampening,
+                             x->weight_decay, x->nesterov, 0, x->st_dev, x->delta, x->word_dev, x->trace_dev,
+                             x->trace_cap, x->group, x->ws_dev, &p.r);
+        if (rc) return rc;
+        const int width = symm_width(p.r.s);
+        p.kernel = step_kernel_any(width, ga, mom, nest);
+        if (!p.kernel)
+            return fail(SS_ERR_CONFIG, "one-launch step: world %d needs multicast (P2P widths 1, 2, 4, 8)",
+                        p.r.s.world);
+        p.kind = ga ? 2 : 1;
+        p.per_thread = ga ? (mom ? 1 : 2) : (mom ? 1 : 2) * SS_STEP_PER_THREAD;
+        p.max_blocks = x->group->max_blocks;
+        p.world = x->group->world;
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p.resident, p.kernel, kThreads, 0) != cudaSuccess ||
+        p.resident <= 0)
+        return check_launch("ss_step_plan_init (occupancy)");
+    p.magic = kPlanMagic;
+    std::memcpy(plan, &p, sizeof(p));
+    return SS_OK;
+}
+
+extern "C" int ss_step_plan_launch(const ss_step_plan* plan, const float* g, float lr, int32_t first_step,
+                                   void* stream) {
+    const PlanImpl* p = reinterpret_cast<const PlanImpl*>(plan);
+    if (!p || p->magic != kPlanMagic) return fail(SS_ERR_CONFIG, "step plan not initialised");
+    if (!(lr >= 0.0f)) return fail(SS_ERR_CONFIG, "learning rate must be non-negative, got %g", (double)lr);
+    RankArgs r = p->r;
+    const int64_t n = r.a.n;
+    if (n > 0 && !g) return fail(SS_ERR_CONFIG, "null gradient pointer");
+    if (p->kind == 2 && g != p->r.a.g) return fail(SS_ERR_CONFIG, "g must be this rank's symmetric buffer");
+    r.a.g = g;
+    r.a.lr = lr;
+    r.a.first = first_step ? 1 : 0;
+    r.a.head = n ? common_head(n, g, r.a.w, r.a.m) : 0;
+    if (p->kind == 1 && r.o.mode != 0 && r.a.head != 0)
+        return fail(SS_ERR_CONFIG, "norm-first order needs 16-byte aligned w, g, m");
+    const int64_t work = (n - r.a.head) / 4 + 1;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (p->kind == 0) {
+        const int grid = static_cast<int>(grid_for(work, p->per_thread, p->resident));
+        r.f.total_blocks = grid;
+        void* params[] = {&r.a, &r.f};
+        (void)launch_ex_c(p->kernel, grid, kThreads, s, false, params);
+        return check_launch("ss_step_plan_launch");
+    }
+    const int grid = step_grid(work, p->per_thread, p->resident, p->max_blocks);
+    r.f.total_blocks = grid;
+    r.o.lag = p->kind == 1 ? static_cast<int>(grid / (p->world + 1) * SS_LAG_SCALE) + 2 : grid / (p->world + 1) + 2;
+    void* params[] = {&r.a, &r.f, &r.s, &r.o};
+    const cudaError_t e = launch_ex_c(p->kernel, grid, kThreads, s, coop_enabled(), params);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return fail(e == cudaErrorCooperativeLaunchTooLarge ? SS_ERR_CONFIG : SS_ERR_CUDA,
+                    "ss_step_plan_launch: %s (grid %d of %d threads: every block must be co-resident)",
+                    cudaGetErrorString(e), grid, kThreads);
+    }
+    return check_launch("ss_step_plan_launch");
 }

@@ -55,16 +55,20 @@ on every rank.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from collections import deque
 from typing import Optional
 
 import torch
 
+from . import _native as N
 from . import kernels as K
 from .collectives import RankGroup, resolve_order
 from .config import SelSyncConfig
 from .errors import ConfigError
+
+_PLAN_LAUNCH = N.LIB.ss_step_plan_launch
 
 
 class SelSyncStep:
@@ -154,6 +158,7 @@ class SelSyncStep:
         self.smoothing = config.smoothing_for(self.world)
         self.signal = K.DeviceSignal(self.device, self.smoothing, config.warmup, trace_capacity)
         self.ws = K.Workspace(self.device)
+        self._fast_cache, self._plans = {}, {}
         self.symm = None
         if self.collective == "symm":
             self.symm = self.comm.make_symmetric(params.numel(), self.device,
@@ -252,41 +257,45 @@ class SelSyncStep:
                 ev[1].record(stream)
 
     def _fast_launch(self, which: str, lr: float, stream) -> None:
-        """Launch K13+K2 (or the one-launch symmetric step) with an argument
-        tuple validated once: only the gradient pointer (the caller may rebind
-        ``grads``), lr, the first-step flag and the stream change per step.
-        At small P a step is shorter than the Python launch path; this keeps
-        that path to one ctypes call."""
-        from . import _native as N
-
+        """Launch K13+K2 (or the one-launch symmetric step) through a prepared
+        step plan (``ss_step_plan_init``: every argument validated once); per
+        step only the gradient pointer (the caller may rebind ``grads``), lr
+        and the first-step flag cross into C, in one 5-argument call. At small
+        P a step is shorter than the host path, so this path is kept short."""
         g = self.grads
-        key = (which, g.data_ptr(), g.numel(), g.dtype, g.device, g.is_contiguous())
-        cache = self.__dict__.setdefault("_fast_cache", {})
-        entry = cache.get(key)
+        key = (which, id(g), g.data_ptr(), g.numel(), self.symm.version if self.symm is not None else 0)
+        entry = self._fast_cache.get(key)
         if entry is None:
-            # full validation whenever a gradient buffer is bound for the first
-            # time (a training loop may rotate a few buffers; each is checked once)
-            K._sgd_check(self.params, self.grads, self.momentum, self.config.momentum)
-            c = self.config
-            m = self.momentum.data_ptr() if self.momentum is not None else None
-            head = [self.params.data_ptr(), self.grads.data_ptr(), m, self.params.numel()]
-            hp = [float(c.momentum), float(c.dampening), float(c.weight_decay), int(bool(c.nesterov))]
-            tail = [self.signal.state.data_ptr(), float(c.delta), self.signal.word.data_ptr(),
-                    self.signal.trace.data_ptr(), self.signal.trace_capacity]
-            if which in ("symm", "symm_ga"):
-                fn = N.LIB.ss_step_symm_f32 if which == "symm" else N.LIB.ss_step_symm_ga_f32
-                tail += [self.symm.group_ref, self.ws.ptr]
-            else:
-                fn = N.LIB.ss_update_norm_signal_f32
-                tail += [self.ws.ptr]
-            if len(cache) >= 16:
-                cache.clear()
-            entry = cache[key] = (fn, head, hp, tail)
-        fn, head, hp, tail = entry
-        rc = fn(*head, lr, *hp, int(self.steps_done == 0), *tail, stream.cuda_stream)
+            entry = self._prepare_launch(which, g, key)
+        rc = _PLAN_LAUNCH(entry[0], entry[1], lr, self.steps_done == 0, stream.cuda_stream)
         if rc:
             N.check(rc)
         K._count()
+
+    def _prepare_launch(self, which: str, g: torch.Tensor, key):
+        # full validation whenever a gradient buffer is bound for the first
+        # time (a training loop may rotate a few buffers; each is checked once);
+        # the entry keeps g alive so its id cannot be reused while cached
+        K._sgd_check(self.params, g, self.momentum, self.config.momentum)
+        pkey = (which, key[-1])
+        plan = self._plans.get(pkey)
+        if plan is None:
+            c = self.config
+            desc = N.RankStepC(
+                self.params.data_ptr(), g.data_ptr(),
+                self.momentum.data_ptr() if self.momentum is not None else None, self.params.numel(),
+                float(c.momentum), float(c.dampening), float(c.weight_decay), int(bool(c.nesterov)),
+                self.signal.state.data_ptr(), float(c.delta), self.signal.word.data_ptr(),
+                self.signal.trace.data_ptr(), self.signal.trace_capacity, 0,
+                ctypes.addressof(self.symm.group_c) if which != "k13" else None, self.ws.ptr)
+            plan = N.StepPlanC()
+            N.check(N.LIB.ss_step_plan_init(ctypes.addressof(plan), ctypes.addressof(desc),
+                                            int(which == "symm_ga")))
+            self._plans = {pkey: plan}  # a group change (new version) drops the old plans
+        if len(self._fast_cache) >= 16:
+            self._fast_cache.clear()
+        entry = self._fast_cache[key] = (ctypes.addressof(plan), g.data_ptr(), g, plan)
+        return entry
 
     def step_async(self, lr: float) -> None:
         """Enqueue one whole step and return without waiting for the GPU.
@@ -363,11 +372,18 @@ class SelSyncStep:
         self._log_step(lr, synced)
         return "sync" if synced else "local"
 
-    def capture(self, lr: float) -> "CapturedStep":
+    def capture(self, lr: float, grads_seq=None) -> "CapturedStep":
         """Record one device-branching step (the gradient buffer bound now, this
         lr) as a CUDA graph; ``replay()`` then equals ``step_async(lr)`` at the
         cost of one graph launch. For launch-bound sizes (small P) and loops
-        that rotate a fixed set of gradient buffers (capture one per buffer)."""
+        that rotate a fixed set of gradient buffers (capture one per buffer).
+
+        ``grads_seq``: a list of gradient buffers -- one graph then holds
+        ``len(grads_seq)`` consecutive steps, step i on ``grads_seq[i]``, and a
+        replay advances the step count by that many. Inside one graph each step
+        kernel is placed on the SMs while the previous one drains (the
+        launches carry programmatic stream serialization), so short steps
+        overlap their launch latency."""
         if not self.async_capable:
             raise ConfigError("capture needs a device-side branch (collective='symm' or a single rank)")
         if self.profile:
@@ -375,13 +391,22 @@ class SelSyncStep:
         if self.steps_done == 0:
             raise ConfigError("run one eager step first (the first step initialises the momentum buffer)")
         lr = self._check_lr(lr)
+        seq = [self.grads] if grads_seq is None else list(grads_seq)
+        if not seq:
+            raise ConfigError("grads_seq must hold at least one gradient buffer")
+        bound = self.grads
         stream = torch.cuda.current_stream(self.device)
         torch.cuda.synchronize(self.device)
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            self._enqueue_device_step(lr, torch.cuda.current_stream(self.device))
+        try:
+            with torch.cuda.graph(graph):
+                for g in seq:
+                    self.grads = g
+                    self._enqueue_device_step(lr, torch.cuda.current_stream(self.device))
+        finally:
+            self.grads = bound
         stream.synchronize()
-        return CapturedStep(self, graph, lr)
+        return CapturedStep(self, graph, lr, len(seq))
 
     # ------------------------------------------------------------------
     def synchronize(self) -> None:
@@ -459,13 +484,14 @@ class SelSyncStep:
 class CapturedStep:
     """A SelSync step recorded as a CUDA graph (``SelSyncStep.capture``)."""
 
-    def __init__(self, step: SelSyncStep, graph, lr: float):
-        self.step, self.graph, self.lr = step, graph, lr
+    def __init__(self, step: SelSyncStep, graph, lr: float, steps: int = 1):
+        self.step, self.graph, self.lr, self.steps = step, graph, lr, steps
 
     def replay(self) -> None:
         self.graph.replay()
-        self.step._log_step(self.lr)
-        K._count()
+        for _ in range(self.steps):
+            self.step._log_step(self.lr)
+            K._count()
 
 
 class TensorListSelSyncStep:

@@ -89,6 +89,40 @@ def test_error_codes_map_to_reference_exceptions():
                                        None, None, 0, None, None, None))
 
 
+def test_step_plan_validates_before_any_launch():
+    """ss_step_plan_init checks what the per-call entry points check; a plan
+    that was never (successfully) initialised refuses to launch."""
+    from paper_2307_07950_b200 import _native as N
+    from paper_2307_07950_b200.errors import ConfigError, SignalError
+
+    plan = N.StepPlanC()
+    with pytest.raises(ConfigError, match="not initialised"):
+        N.check(N.LIB.ss_step_plan_launch(ctypes.addressof(plan), 16, 0.1, 0, None))
+    with pytest.raises(ConfigError):
+        N.check(N.LIB.ss_step_plan_init(None, None, 0))
+    st = N.SignalStateC()
+    desc = N.RankStepC(16, 32, 48, 100, 0.9, 0.0, 4e-4, 0, ctypes.addressof(st), 0.3, 64, None, 0, 0, None, 80)
+    cases = [
+        (dict(momentum=-1.0), ConfigError),            # make_sgd_args
+        (dict(nesterov=1, dampening=0.5), ConfigError),
+        (dict(m=None), ConfigError),                   # momentum buffer required
+        (dict(delta=-0.5), SignalError),               # DeltaThreshold
+        (dict(trace=96, trace_cap=0), ConfigError),
+        (dict(ws=None), ConfigError),
+    ]
+    for change, exc in cases:
+        d = N.RankStepC.from_buffer_copy(desc)
+        for k, v in change.items():
+            setattr(d, k, v)
+        with pytest.raises(exc):
+            N.check(N.LIB.ss_step_plan_init(ctypes.addressof(plan), ctypes.addressof(d), 0))
+        with pytest.raises(ConfigError, match="not initialised"):  # a failed init leaves no plan
+            N.check(N.LIB.ss_step_plan_launch(ctypes.addressof(plan), 16, 0.1, 0, None))
+    # gradient aggregation needs a symmetric group
+    with pytest.raises(ConfigError, match="symmetric group"):
+        N.check(N.LIB.ss_step_plan_init(ctypes.addressof(plan), ctypes.addressof(desc), 1))
+
+
 def test_build_flags_target_sm100a():
     from paper_2307_07950_b200 import _build
 

@@ -178,6 +178,37 @@ def test_captured_steps_match_oracle():
         SelSyncStep(w.clone(), bufs[0], SelSyncConfig(delta=delta, warmup=warmup)).capture(lr)
 
 
+@pytest.mark.parametrize("per_graph", [3, 13])
+def test_multi_step_graphs_match_oracle(per_graph):
+    """capture(lr, grads_seq): several consecutive steps in one CUDA graph
+    (programmatic dependent launch between the step kernels inside it), the
+    remainder as one-step graphs -- same trace and parameters as the oracle."""
+    d, steps, seed, delta, warmup, lr = 3000, 40, 17, 0.003, 2, 0.1
+    P = 2 * d + 2
+    init = O.init_params_linear(d, 5).astype(np.float32).astype(np.float64)
+    w = torch.tensor(init, dtype=torch.float32, device=DEV)
+    bufs = [torch.tensor(O.synthetic_grad32(seed, 0, s, P), dtype=torch.float32, device=DEV) for s in range(steps)]
+    step = SelSyncStep(w, bufs[0], SelSyncConfig(delta=delta, warmup=warmup, momentum=0.9, weight_decay=4e-4))
+    step.step_async(lr)
+    graphs, s = [], 1
+    while s < steps:
+        k = min(per_graph, steps - s)
+        graphs.append(step.capture(lr, bufs[s:s + k]))
+        s += k
+    assert step.steps_done == 1 and step.grads is bufs[0]
+    for gr in graphs:
+        gr.replay()
+    step.synchronize()
+    assert step.steps_done == steps
+    ref = O.simulate_selsync(init, 1, steps, lambda w_, s, _p: O.synthetic_grad32(seed, 0, s, P),
+                             delta=delta, warmup=warmup, lr=lr, momentum=0.9, weight_decay=4e-4)
+    assert 0 < ref.decision.sum() < steps
+    assert_trace_parity(step.decisions(), ref.decision, ref.delta_g, delta, warmup)
+    params_close(w.double().cpu().numpy(), ref.finals[0])
+    with pytest.raises(ConfigError):
+        step.capture(lr, [])
+
+
 @pytest.mark.parametrize("order", ["update_first", "norm_first", "adaptive"])
 def test_single_rank_symmetric_step_matches_oracle(order, tmp_path):
     """The one-launch symmetric-memory step on one rank (world-1 group, the
