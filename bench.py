@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--graph", action="store_true",
                     help="model workloads: capture fwd + bwd + SelSync step in one CUDA graph; microbench: "
                          "replay captured steps (launch-bound small P)")
-    ap.add_argument("--graph-steps", type=int, default=4,
+    ap.add_argument("--graph-steps", type=int, default=1,
                     help="microbench --graph: consecutive steps per captured graph (the gradient ring in order; "
                          "remainders replay one-step graphs)")
     ap.add_argument("--sel-warmup", type=int, default=25, help="EWMA window / warmup for model workloads")

@@ -156,8 +156,8 @@ __host__ __device__ inline bool sync_proven_early_core(const ss_signal_state* st
     return rel_change_core(s.ewma_previous, s.ewma_current) >= delta;
 }
 
-// K2 body: one thread. Writes the flag word and the trace row.
-__device__ void signal_step_dev(ss_signal_state* st, double x, double delta, int32_t* word,
+// K2 body: one thread. Writes the flag word and the trace row; returns the word.
+__device__ int signal_step_dev(ss_signal_state* st, double x, double delta, int32_t* word,
                                 ss_trace_row* trace, int32_t cap) {
     ss_signal_state s = *st;
     int err = observe_core(&s, x);
@@ -178,6 +178,7 @@ __device__ void signal_step_dev(ss_signal_state* st, double x, double delta, int
     }
     if (word) *word = row.word;
     if (trace && cap > 0) trace[row.step % cap] = row;
+    return row.word;
 }
 
 // ----------------------------------------------------- memory helpers
@@ -273,6 +274,15 @@ __device__ void finish_norm(const Finish& f, double acc, VBlk vb) {
     __shared__ bool s_last;
     Workspace ws = ws_view(f.ws);
     double bsum = block_sum(acc);
+    if (f.total_blocks == 1) {
+        // the only block is the last one: no partials round trip (same value:
+        // the two-pass sum of one partial and zeros is exact)
+        if (threadIdx.x == 0) {
+            if (f.out) *f.out = bsum;
+            if (f.st) signal_step_dev(f.st, bsum, f.delta, f.word, f.trace, f.cap);
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
         ws.partials[f.block_offset + vb.bid] = bsum;
         __threadfence();

@@ -114,6 +114,9 @@ constexpr int kNormFirst = 1, kKnown = 2, kSafe = 4;
 __device__ __forceinline__ void red_add_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_add_relaxed_sys(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
     uint32_t v;
@@ -172,12 +175,14 @@ __device__ bool poisoned(const SymmArgs& s, uint64_t seq) {
 }
 
 __device__ void post_poison(const SymmArgs& s, uint64_t seq) {
-    for (int j = 0; j < s.world; ++j) st_release_sys(poison_slot(s, j, s.rank), seq);
+    fence_acq_rel_sys();
+    for (int j = 0; j < s.world; ++j) st_relaxed_sys(poison_slot(s, j, s.rank), seq);
 }
 
 // end of a sync step on this rank: done tags to every peer, wait for all
 __device__ void end_barrier(const SymmArgs& s, uint64_t seq) {
-    for (int j = 0; j < s.world; ++j) st_release_sys(done_slot(s, j, s.rank), seq);
+    fence_acq_rel_sys();
+    for (int j = 0; j < s.world; ++j) st_relaxed_sys(done_slot(s, j, s.rank), seq);
     bool to = false;
     for (int j = 0; j < s.world && !to; ++j) wait_tag(done_slot(s, s.rank, j), seq, 0, s, &to);
     if (to) atomicExch(s.err, SS_SYMM_ERR_TIMEOUT);
@@ -249,10 +254,11 @@ __device__ void known_tile_done(const Finish& f, const SymmArgs& s, const Overla
         // K2 advances step_count, which every block reads once at kernel start
         // to pick this launch's order: run it only after all of them have
         wait_count_gpu(o.started, static_cast<unsigned int>(vb.n), s);
-        signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
-        const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+        const int own = signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+        const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(own);
         vote_fence();
-        for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
+        fence_acq_rel_sys();
+        for (int j = 0; j < N; ++j) st_relaxed_sys(vote_slot(s, j, seq, s.rank), tagged);
         if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
     }
 }
@@ -337,7 +343,8 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                     prev = cum;
                     if (ld_relaxed_gpu(o.early_posted) != seq && sync_proven_early_core(f.st, lower, f.delta)) {
                         *reinterpret_cast<volatile uint64_t*>(o.early_posted) = seq;
-                        for (int j = 0; j < N; ++j) st_release_sys(early_slot(s, j, s.rank), seq);
+                        fence_acq_rel_sys();
+                        for (int j = 0; j < N; ++j) st_relaxed_sys(early_slot(s, j, s.rank), seq);
                         if (o.dbg) o.dbg[4 * o.dbg_cap + 3] = now_ns();
                     }
                 }
@@ -360,10 +367,11 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
             if (threadIdx.x == 0) {
                 *ws.counter = 0u;
                 if (early) *o.running = 0.0;  // every block has added its partial
-                signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
-                const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+                const int own = signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+                const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(own);
                 vote_fence();
-                for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
+                fence_acq_rel_sys();
+                for (int j = 0; j < N; ++j) st_relaxed_sys(vote_slot(s, j, seq, s.rank), tagged);
                 if (o.dbg) o.dbg[4 * o.dbg_cap + 1] = now_ns();
             }
         }
@@ -508,25 +516,33 @@ __device__ __forceinline__ void uf_body(const SgdArgs& a, const Finish& f, const
     Workspace ws = ws_view(f.ws);
     const double bsum = block_sum(acc);
     if (threadIdx.x == 0) {
-        ws.partials[vb.bid] = bsum;
-        // gpu scope suffices: the last block observes this counter, then
-        // releases the vote at system scope (causality is transitive), so
-        // peers reading after the vote see these stores
-        __threadfence();
-        s_last = atomicAdd(ws.counter, 1u) == static_cast<unsigned int>(vb.n - 1);
+        if (vb.n == 1) {
+            s_last = true;  // one block (small P): no partials round trip
+        } else {
+            ws.partials[vb.bid] = bsum;
+            // gpu scope suffices: the last block observes this counter, then
+            // releases the vote at system scope (causality is transitive), so
+            // peers reading after the vote see these stores
+            __threadfence();
+            s_last = atomicAdd(ws.counter, 1u) == static_cast<unsigned int>(vb.n - 1);
+        }
     }
     __syncthreads();
     if (s_last) {
-        __threadfence();
-        double v = 0.0;
-        for (int i = threadIdx.x; i < vb.n; i += blockDim.x) v += __ldcg(ws.partials + i);
-        v = block_sum(v);
+        double v = bsum;  // thread 0's value counts
+        if (vb.n > 1) {
+            __threadfence();
+            v = 0.0;
+            for (int i = threadIdx.x; i < vb.n; i += blockDim.x) v += __ldcg(ws.partials + i);
+            v = block_sum(v);
+        }
         if (threadIdx.x == 0) {
             *ws.counter = 0u;
-            signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
-            const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+            const int own = signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+            const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(own);
             vote_fence();
-            for (int j = 0; j < s.world; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
+            fence_acq_rel_sys();
+            for (int j = 0; j < s.world; ++j) st_relaxed_sys(vote_slot(s, j, seq, s.rank), tagged);
             if (mark) mark[1] = now_ns();
             const int w = agreed_vote(s, seq);
             if (mark) mark[2] = now_ns();
@@ -620,10 +636,11 @@ __device__ __forceinline__ void ga_body(const SgdArgs& a, const Finish& f, const
             v = block_sum(v);
             if (threadIdx.x == 0) {
                 *ws.counter = 0u;
-                signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
-                const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(*f.word);
+                const int own = signal_step_dev(f.st, v, f.delta, f.word, f.trace, f.cap);
+                const uint64_t tagged = (seq << 32) | static_cast<uint32_t>(own);
                 vote_fence();
-                for (int j = 0; j < N; ++j) st_release_sys(vote_slot(s, j, seq, s.rank), tagged);
+                fence_acq_rel_sys();
+                for (int j = 0; j < N; ++j) st_relaxed_sys(vote_slot(s, j, seq, s.rank), tagged);
             }
         }
     }
@@ -656,8 +673,10 @@ __device__ __forceinline__ void ga_body(const SgdArgs& a, const Finish& f, const
                 const int64_t e0 = t * o.tile, e1 = e0 + o.tile < a.n ? e0 + o.tile : a.n;
                 average_block_range<W>(s, e0, e1);
                 __syncthreads();
-                if (threadIdx.x == 0)
-                    for (int j = 0; j < N; ++j) red_add_release_sys(o.cnt[j] + t, 1u);
+                if (threadIdx.x == 0) {
+                    fence_acq_rel_sys();
+                    for (int j = 0; j < N; ++j) red_add_relaxed_sys(o.cnt[j] + t, 1u);
+                }
             }
         } else {
             // ---- update tile t of group grp - lag (owner t % N), with the mean gradient on sync

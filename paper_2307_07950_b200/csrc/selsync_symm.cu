@@ -58,9 +58,9 @@ __global__ void __launch_bounds__(kThreads, SS_SYMM_MINB) symm_sync_kernel(SymmA
         if (a.exchange) {
             if (blockIdx.x == 0) {
                 const int own = *a.word;
-                __threadfence_system();
                 const uint64_t v = (seq << 32) | static_cast<uint32_t>(own);
-                for (int j = 0; j < a.world; ++j) st_release_sys(vote_slot(a, j, seq, a.rank), v);
+                fence_acq_rel_sys();
+                for (int j = 0; j < a.world; ++j) st_relaxed_sys(vote_slot(a, j, seq, a.rank), v);
             }
             w = 0;
             for (int j = 0; j < a.world && !timed_out; ++j) {
@@ -89,7 +89,8 @@ __global__ void __launch_bounds__(kThreads, SS_SYMM_MINB) symm_sync_kernel(SymmA
             if (a.exchange) *a.word = w;
             if (a.agreed_ring && a.ring_cap > 0) a.agreed_ring[(seq - 1) % a.ring_cap] = s_timeout ? -1 : w;
             if (sync) {
-                for (int j = 0; j < a.world; ++j) st_release_sys(done_slot(a, j, a.rank), seq);
+                fence_acq_rel_sys();
+                for (int j = 0; j < a.world; ++j) st_relaxed_sys(done_slot(a, j, a.rank), seq);
                 bool timed_out = false;
                 for (int j = 0; j < a.world && !timed_out; ++j) wait_tag(done_slot(a, a.rank, j), seq, 0, a, &timed_out);
                 if (timed_out) atomicExch(a.err, SS_SYMM_ERR_TIMEOUT);

@@ -1,19 +1,21 @@
 #!/bin/bash
 # BASELINE configs[4]: flattened parameter sweep 1M-1B, forced all-local / all-sync
-# and the 50% mix, at N in $NS (default "1 2 4"). P <= 16M replays one CUDA graph
-# per step at N = 1 (launch-bound sizes); everything else uses the host launch path.
+# and the 50% mix, at N in $NS (default "1 2 4"). P <= 2M replays one CUDA graph
+# per step at N = 1 (host-bound there); everything else uses the host launch path
+# (prepared step plans + programmatic dependent launch: faster than graph
+# replays from 4M up, profiles/r02_plan/, profiles/r02_pdl/).
 NS=${NS:-"1 2 4"}
 SIZES=${SIZES:-"1000000 4000000 16000000 64000000 100000000 256000000 1000000000"}
 mkdir -p gpurun_out/sweep
 for P in $SIZES; do
-  # graph replay only at N = 1: at N > 1 eager cooperative launches measured faster
-  # (profiles/r02_small_p/max_blocks_n2.txt)
-  G=""; [ "$P" -le 16000000 ] && G="--graph"
-  # and at N > 1 without per-launch events there (they cost a few us per step)
+  # graph replay only at N = 1 and P <= 2M: at N > 1 eager cooperative launches
+  # measured faster (profiles/r02_small_p/max_blocks_n2.txt)
+  G=""; [ "$P" -le 2000000 ] && G="--graph"
+  # no per-launch events up to 16M (they cost a few us per step)
   E=""; [ "$P" -le 16000000 ] && E="--no-kernel-events"
   for N in $NS; do
     if [ "$N" = "1" ]; then
-      timeout 600 python bench.py --P $P --steps 50 --warmup 5 --no-e2e --no-cpu-baseline $G \
+      timeout 600 python bench.py --P $P --steps 50 --warmup 5 --no-e2e --no-cpu-baseline ${G:-$E} \
         > gpurun_out/sweep/n1_$P.json 2> gpurun_out/sweep/n1_$P.err
     else
       timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
