@@ -63,6 +63,14 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 #ifndef SS_NVLS_U
 #define SS_NVLS_U 4
 #endif
+// 16-byte vectors in flight per thread in the per-tile means of the
+// overlapped sync step (one block per tile): NVLS reductions, P2P vectors per rank
+#ifndef SS_TILE_U_NVLS
+#define SS_TILE_U_NVLS 2
+#endif
+#ifndef SS_TILE_U_P2P
+#define SS_TILE_U_P2P 2
+#endif
 
 __device__ __forceinline__ float4 mm_ld_reduce_add4(const float* p) {
     float4 v;
@@ -199,18 +207,21 @@ __device__ void average_block_range(const SymmArgs& a_in, int64_t e0, int64_t e1
     for (int r = 0; r < (W > 0 ? W : 1); ++r) a.bufs[r] = a_in.bufs[r];
     const int64_t v0 = e0 >> 2, v1 = e1 >> 2;
     if constexpr (W == 0) {
+        constexpr int U = SS_TILE_U_NVLS;  // multimem reductions in flight per thread
+        const int64_t bs = blockDim.x;
         int64_t i = v0 + threadIdx.x;
-        for (; i + blockDim.x < v1; i += 2 * blockDim.x) {
-            float4 x = mm_ld_reduce_add4(a.mc + 4 * i);
-            float4 y = mm_ld_reduce_add4(a.mc + 4 * (i + blockDim.x));
-            mm_st4(a.mc + 4 * i, scale4(x, a.scale));
-            mm_st4(a.mc + 4 * (i + blockDim.x), scale4(y, a.scale));
+        for (; i + (U - 1) * bs < v1; i += U * bs) {
+            float4 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = mm_ld_reduce_add4(a.mc + 4 * (i + u * bs));
+#pragma unroll
+            for (int u = 0; u < U; ++u) mm_st4(a.mc + 4 * (i + u * bs), scale4(x[u], a.scale));
         }
-        for (; i < v1; i += blockDim.x) mm_st4(a.mc + 4 * i, scale4(mm_ld_reduce_add4(a.mc + 4 * i), a.scale));
+        for (; i < v1; i += bs) mm_st4(a.mc + 4 * i, scale4(mm_ld_reduce_add4(a.mc + 4 * i), a.scale));
         for (int64_t j = 4 * v1 + threadIdx.x; j < e1; j += blockDim.x)
             mm_st1(a.mc + j, mm_ld_reduce_add1(a.mc + j) * a.scale);
     } else {
-        constexpr int U = W <= 4 ? 2 : 1;  // peer loads in flight per thread: U * W
+        constexpr int U = W <= 2 ? SS_TILE_U_P2P : (W <= 4 ? 2 : 1);  // peer loads in flight per thread: U * W
         const int64_t bs = blockDim.x;
         int64_t i = v0 + threadIdx.x;
         for (; i + (U - 1) * bs < v1; i += U * bs) {
