@@ -210,3 +210,45 @@ def test_full_size_properties(P):
     idx = torch.randint(0, P, (100_000,), generator=gen, device=DEV)
     want = w0[idx].double() - 0.125 * g[idx].double()
     torch.testing.assert_close(w[idx].double(), want, rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("offset,mom,nest,n", [(0, 0.9, 0, 300_007), (1, 0.9, 0, 300_007), (3, 0.0, 0, 65_541),
+                                               (0, 0.9, 1, 1_002), (2, 0.9, 0, 1_000_003)])
+def test_step_plan_is_bit_identical_to_the_per_call_entry_point(offset, mom, nest, n):
+    """ss_step_plan_init/launch (the per-step path of SelSyncStep) and
+    ss_update_norm_signal_f32 (every argument per call) on the same inputs:
+    the same parameters, momentum, votes and trace rows, bit for bit --
+    misaligned heads, the one-block grid (n = 1,002) and ragged tails included."""
+    import ctypes
+
+    lr, wd, delta = 0.05, 4e-4, 0.2  # the step-4 Delta (0.07) is local, the rest sync
+    w0 = rand32(n, 1, 0.1)
+    grads = [dev_view(rand32(n, 10 + s, 1.0 + 0.3 * (s % 3)), offset) for s in range(7)]
+    runs = []
+    for use_plan in (False, True):
+        w = dev_view(w0, offset)
+        m = dev_view(np.zeros(n, np.float32), offset)
+        sig = K.DeviceSignal(DEV, 0.5, 2, 64)
+        ws = K.Workspace(DEV)
+        stream = torch.cuda.current_stream().cuda_stream
+        if use_plan:
+            desc = N.RankStepC(w.data_ptr(), grads[0].data_ptr(), m.data_ptr() if mom else None, n, mom, 0.0, wd,
+                               nest, sig.state.data_ptr(), delta, sig.word.data_ptr(), sig.trace.data_ptr(), 64, 0,
+                               None, ws.ptr)
+            plan = N.StepPlanC()
+            N.check(N.LIB.ss_step_plan_init(ctypes.addressof(plan), ctypes.addressof(desc), 0))
+        words = []
+        for s, g in enumerate(grads):
+            if use_plan:
+                N.check(N.LIB.ss_step_plan_launch(ctypes.addressof(plan), g.data_ptr(), lr, int(s == 0), stream))
+            else:
+                K.update_norm_signal_(w, g, m if mom else None, sig, ws, lr=lr, delta=delta, momentum=mom,
+                                      weight_decay=wd, nesterov=bool(nest), first_step=s == 0)
+            words.append(int(sig.word.item()))
+        torch.cuda.synchronize()
+        runs.append((w.cpu().numpy().copy(), m.cpu().numpy().copy(), words, sig.read_trace()[:7].tobytes()))
+    (wa, ma, da, ta), (wb, mb, db, tb) = runs
+    assert np.array_equal(wa.view(np.uint32), wb.view(np.uint32))
+    assert np.array_equal(ma.view(np.uint32), mb.view(np.uint32))
+    assert da == db and 0 < sum(x & 1 for x in da) < len(da)
+    assert ta == tb
