@@ -1173,13 +1173,16 @@ extern "C" int ss_step_plan_init(ss_step_plan* plan, const ss_rank_step* x, int3
 
 extern "C" int ss_step_plan_launch(const ss_step_plan* plan, const float* g, float lr, int32_t first_step,
                                    void* stream) {
-    const PlanImpl* p = reinterpret_cast<const PlanImpl*>(plan);
-    if (!p || p->magic != kPlanMagic) return fail(SS_ERR_CONFIG, "step plan not initialised");
+    if (!plan) return fail(SS_ERR_CONFIG, "step plan not initialised");
+    PlanImpl pl;  // a copy: the caller's storage is plain words (no aliasing through it)
+    std::memcpy(&pl, plan, sizeof(pl));
+    const PlanImpl* p = &pl;
+    if (p->magic != kPlanMagic) return fail(SS_ERR_CONFIG, "step plan not initialised");
     if (!(lr >= 0.0f)) return fail(SS_ERR_CONFIG, "learning rate must be non-negative, got %g", (double)lr);
-    RankArgs r = p->r;
+    RankArgs& r = pl.r;
     const int64_t n = r.a.n;
     if (n > 0 && !g) return fail(SS_ERR_CONFIG, "null gradient pointer");
-    if (p->kind == 2 && g != p->r.a.g) return fail(SS_ERR_CONFIG, "g must be this rank's symmetric buffer");
+    if (p->kind == 2 && g != r.a.g) return fail(SS_ERR_CONFIG, "g must be this rank's symmetric buffer");
     r.a.g = g;
     r.a.lr = lr;
     r.a.first = first_step ? 1 : 0;
