@@ -94,6 +94,17 @@ def parse():
     return ap.parse_args()
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (the baseline's hardware, stated with its core count)."""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -205,6 +216,7 @@ def cpu_run(n_workers, P, steps, warmup, args, budget_s):
         "unit": "steps/s",
         "cores": threads,
         "host_cpus": os.cpu_count(),
+        "cpu_model": cpu_model(),
         "kind": "port",
         "sample": (f"{steps} timed steps of the reference's float64 SelSync step (oracle/cpu_path.py: "
                    f"g@g, observe/decide, SGD+momentum+wd, flag OR, on sync f64 serialize + PS "
@@ -235,7 +247,7 @@ def reference_arm(args, rank, world):
         "dtype": "fp64",
         "data": "synthetic",
         "config": workload_config(args, world),
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "host_cpus", "kind", "sample")},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "host_cpus", "cpu_model", "kind", "sample")},
         "e2e": {"value": base["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -587,7 +599,8 @@ def main():
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_run(1, P, 3, 1, args, args.cpu_seconds)
-        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "host_cpus", "kind", "sample")}
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "host_cpus", "cpu_model", "kind",
+                                                    "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
