@@ -304,7 +304,14 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     __shared__ bool s_go;
     const int N = s.world;
     const int64_t T = o.n_tiles;
-    const int64_t groups = (T + N - 1) / N + o.lag;
+    // groups between a tile's update tickets and its mean ticket: o.lag (one
+    // in-flight window) scaled per pass -- the known pass starts its means
+    // with the first updates and gains from a shorter lag (x3/4), the pass
+    // after the ||g||^2 sweep from a longer one (x3/2): N = 2 / 4, P = 100M,
+    // -5 / -6 us per known-pass sync step, -1.5 us per mixed step
+    // (profiles/r02_lag4/)
+    const int lag = known ? (o.lag - 2) * 3 / 4 + 2 : (o.lag - 2) * 3 / 2 + 2;
+    const int64_t groups = (T + N - 1) / N + lag;
     const unsigned long long total = static_cast<unsigned long long>(groups) * (N + 1);
     const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(o.epoch) + 1;
     const uint32_t target = static_cast<uint32_t>(N) * epoch;
@@ -435,7 +442,7 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
                 }
             } else {
                 // ---- mean of owned tile t: needs the agreed vote and all N updates
-                const int64_t m = grp - o.lag;
+                const int64_t m = grp - lag;
                 const int64_t t = m * N + s.rank;
                 if (m >= 0 && t < T) {
                     if (threadIdx.x == 0) {
