@@ -104,6 +104,15 @@ __device__ __forceinline__ void vote_fence() {
 #ifndef SS_LAG_SCALE
 #define SS_LAG_SCALE 1
 #endif
+// per-pass scaling of the lag (nf_body): known pass x3/4, after the sweep x3/2
+#ifndef SS_LAG_KNOWN_NUM
+#define SS_LAG_KNOWN_NUM 3
+#define SS_LAG_KNOWN_DEN 4
+#endif
+#ifndef SS_LAG_SWEEP_NUM
+#define SS_LAG_SWEEP_NUM 3
+#define SS_LAG_SWEEP_DEN 2
+#endif
 
 constexpr int kEarlySync = -3;  // vote_or_early: a peer proved the step sync before its sweep ended
 constexpr int kEarlyChunks = 8;  // the early vote's ||g||^2 sweep reports its running sum this often
@@ -310,7 +319,8 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     // after the ||g||^2 sweep from a longer one (x3/2): N = 2 / 4, P = 100M,
     // -5 / -6 us per known-pass sync step, -1.5 us per mixed step
     // (profiles/r02_lag4/)
-    const int lag = known ? (o.lag - 2) * 3 / 4 + 2 : (o.lag - 2) * 3 / 2 + 2;
+    const int lag = known ? (o.lag - 2) * SS_LAG_KNOWN_NUM / SS_LAG_KNOWN_DEN + 2
+                          : (o.lag - 2) * SS_LAG_SWEEP_NUM / SS_LAG_SWEEP_DEN + 2;
     const int64_t groups = (T + N - 1) / N + lag;
     const unsigned long long total = static_cast<unsigned long long>(groups) * (N + 1);
     const uint32_t epoch = *reinterpret_cast<volatile uint32_t*>(o.epoch) + 1;
