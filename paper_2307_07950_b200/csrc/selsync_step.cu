@@ -104,7 +104,7 @@ __device__ __forceinline__ void vote_fence() {
 #ifndef SS_LAG_SCALE
 #define SS_LAG_SCALE 1
 #endif
-// per-pass scaling of the lag (nf_body): known pass x3/4, after the sweep x3/2
+// per-pass scaling of the lag (nf_body): known pass x3/4 (P2P widths), after the sweep x3/2
 #ifndef SS_LAG_KNOWN_NUM
 #define SS_LAG_KNOWN_NUM 3
 #define SS_LAG_KNOWN_DEN 4
@@ -314,12 +314,14 @@ __device__ __forceinline__ void nf_body(const SgdArgs& a, const Finish& f, const
     const int N = s.world;
     const int64_t T = o.n_tiles;
     // groups between a tile's update tickets and its mean ticket: o.lag (one
-    // in-flight window) scaled per pass -- the known pass starts its means
-    // with the first updates and gains from a shorter lag (x3/4), the pass
-    // after the ||g||^2 sweep from a longer one (x3/2): N = 2 / 4, P = 100M,
-    // -5 / -6 us per known-pass sync step, -1.5 us per mixed step
+    // in-flight window) scaled per pass -- the pass after the ||g||^2 sweep
+    // meets its updates already streaming and gains from a longer lag (x3/2:
+    // -1.4 to -1.7 us per mixed step at N = 2 and 4); the known pass starts
+    // its means with the first updates, and over P2P (N = 2) a shorter lag
+    // (x3/4) gains 5-7 us per sync step, while over NVLS (N = 4) two same-box
+    // A/Bs disagree in sign (+-6 us), so NVLS keeps the base lag
     // (profiles/r02_lag4/)
-    const int lag = known ? (o.lag - 2) * SS_LAG_KNOWN_NUM / SS_LAG_KNOWN_DEN + 2
+    const int lag = known ? (W == 0 ? o.lag : (o.lag - 2) * SS_LAG_KNOWN_NUM / SS_LAG_KNOWN_DEN + 2)
                           : (o.lag - 2) * SS_LAG_SWEEP_NUM / SS_LAG_SWEEP_DEN + 2;
     const int64_t groups = (T + N - 1) / N + lag;
     const unsigned long long total = static_cast<unsigned long long>(groups) * (N + 1);
