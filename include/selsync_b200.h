@@ -388,6 +388,10 @@ typedef struct ss_step_plan {
 SS_API int ss_step_plan_init(ss_step_plan* plan_host, const ss_rank_step* rank_host, int32_t grads);
 SS_API int ss_step_plan_launch(const ss_step_plan* plan_host, const float* g_dev, float lr, int32_t first_step,
                                void* stream);
+/* Compiled field offsets of ss_rank_step in declaration order, then
+   sizeof(ss_rank_step) and sizeof(ss_step_plan): lets a binding check its
+   mirror of the structs (host-only, no GPU). */
+SS_API int ss_rank_step_layout(int64_t* offsets_host, int32_t cap, int32_t* count_host);
 
 #ifdef __cplusplus
 }

@@ -180,6 +180,7 @@ _SIGS = {
     "ss_colocated_args_bytes": ([c_int32, POINTER(c_int64)], c_int),
     "ss_colocated_prepare_f32": ([c_void_p, c_int32, c_int32, c_int32, c_void_p, c_void_p], c_int),
     "ss_colocated_step_f32": ([c_void_p, c_float, c_int32, c_void_p], c_int),
+    "ss_rank_step_layout": ([POINTER(c_int64), c_int32, POINTER(c_int32)], c_int),
     "ss_step_plan_init": ([c_void_p, c_void_p, c_int32], c_int),
     "ss_step_plan_launch": ([c_void_p, c_void_p, c_float, c_int32, c_void_p], c_int),
     "ss_step_symm_f32": (

@@ -144,6 +144,25 @@ int ss_symm_group_layout(int64_t* offsets, int32_t cap, int32_t* count) {
     return SS_OK;
 }
 
+int ss_rank_step_layout(int64_t* offsets, int32_t cap, int32_t* count) {
+    const int64_t o[] = {
+        (int64_t)offsetof(ss_rank_step, w_dev),        (int64_t)offsetof(ss_rank_step, g_dev),
+        (int64_t)offsetof(ss_rank_step, m_dev),        (int64_t)offsetof(ss_rank_step, n),
+        (int64_t)offsetof(ss_rank_step, momentum),     (int64_t)offsetof(ss_rank_step, dampening),
+        (int64_t)offsetof(ss_rank_step, weight_decay), (int64_t)offsetof(ss_rank_step, nesterov),
+        (int64_t)offsetof(ss_rank_step, st_dev),       (int64_t)offsetof(ss_rank_step, delta),
+        (int64_t)offsetof(ss_rank_step, word_dev),     (int64_t)offsetof(ss_rank_step, trace_dev),
+        (int64_t)offsetof(ss_rank_step, trace_cap),    (int64_t)offsetof(ss_rank_step, reserved),
+        (int64_t)offsetof(ss_rank_step, group),        (int64_t)offsetof(ss_rank_step, ws_dev),
+        (int64_t)sizeof(ss_rank_step),                 (int64_t)sizeof(ss_step_plan)};
+    const int32_t n = static_cast<int32_t>(sizeof(o) / sizeof(o[0]));
+    if (!offsets || !count) return fail(SS_ERR_CONFIG, "null argument");
+    if (cap < n) return fail(SS_ERR_CONFIG, "layout needs %d entries, got room for %d", n, cap);
+    for (int32_t i = 0; i < n; ++i) offsets[i] = o[i];
+    *count = n;
+    return SS_OK;
+}
+
 int ss_symm_signal_bytes(int32_t world, int64_t* bytes) {
     if (!bytes) return fail(SS_ERR_CONFIG, "null output");
     if (world < 1 || world > kMaxRanks) return fail(SS_ERR_CONFIG, "world size must be in [1, %d], got %d", kMaxRanks, world);

@@ -89,6 +89,20 @@ def test_error_codes_map_to_reference_exceptions():
                                        None, None, 0, None, None, None))
 
 
+def test_rank_step_layout_matches_ctypes_mirror():
+    """ss_rank_step's compiled field offsets and size, and the size of the
+    opaque ss_step_plan, equal the ctypes mirrors the package builds plans from."""
+    from paper_2307_07950_b200 import _native as N
+
+    offs = (ctypes.c_int64 * 32)()
+    count = ctypes.c_int32(0)
+    N.check(N.LIB.ss_rank_step_layout(offs, 32, ctypes.byref(count)))
+    names = [f[0] for f in N.RankStepC._fields_]
+    want = [getattr(N.RankStepC, n).offset for n in names] + [ctypes.sizeof(N.RankStepC),
+                                                              ctypes.sizeof(N.StepPlanC)]
+    assert list(offs[: count.value]) == want
+
+
 def test_step_plan_validates_before_any_launch():
     """ss_step_plan_init checks what the per-call entry points check; a plan
     that was never (successfully) initialised refuses to launch."""
