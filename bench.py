@@ -325,14 +325,16 @@ def main():
     g = torch.empty(P, device=dev)
     mom = torch.zeros(P, device=dev)
 
-    def make_step(delta, smoothing=1.0):
+    def make_step(delta, smoothing=1.0, events=True):
+        """events: CUDA events around every launch (the per-kernel times of the
+        roofline); the headline run goes without them, back to back."""
         cfg = SelSyncConfig(delta=delta, warmup=1, smoothing=smoothing, momentum=args.momentum,
                             weight_decay=args.weight_decay)
         st = SelSyncStep(w, g, cfg, momentum_buffer=mom, group=comm, fuse=not args.no_fuse,
                          collective=args.collective if world > 1 else None,
                          flag_exchange=(args.flag_exchange if args.collective == "symm" else "nccl"),
-                         trace_capacity=1 << 14, profile=not (args.graph or args.no_kernel_events), order=args.order, tile_elems=args.tile,
-                         early_vote=args.early_vote)
+                         trace_capacity=1 << 14, profile=events and not (args.graph or args.no_kernel_events),
+                         order=args.order, tile_elems=args.tile, early_vote=args.early_vote)
         return st
 
     captured = {}  # --graph: one CUDA graph per (step object, gradient buffer)
@@ -431,7 +433,7 @@ def main():
         from paper_2307_07950_b200.errors import TransportError
 
         try:
-            mixed = make_step(0.3)
+            mixed = make_step(0.3, events=False)
             run(mixed, args.warmup)
             mixed.synchronize()
         except (TransportError, RuntimeError) as exc:
@@ -440,10 +442,10 @@ def main():
             print(f"bench: symmetric-memory path failed on some rank ({failure}); falling back to NCCL",
                   file=sys.stderr, flush=True)
             args.collective = "nccl"
-            mixed = make_step(0.3)
+            mixed = make_step(0.3, events=False)
             run(mixed, args.warmup)
     else:
-        mixed = make_step(0.3)
+        mixed = make_step(0.3, events=False)
         run(mixed, args.warmup)
     clocks.start()
     res = timed(mixed, args.steps)
