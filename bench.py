@@ -105,6 +105,31 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def bind_host_to_gpu(index: int):
+    """Bind this process to the CPUs NVML lists as closest to GPU `index` (its
+    NUMA node) while the e2e arm allocates its pinned host buffers, so its H2D
+    copies read memory local to the GPU. SS_BENCH_NUMA=0 skips it. Returns
+    the CPU count bound to, or None."""
+    if os.environ.get("SS_BENCH_NUMA", "1") == "0":
+        return None
+    try:
+        import pynvml
+        import torch
+
+        pr = torch.cuda.get_device_properties(index)
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = [64 * w + b for w, word in enumerate(words) for b in range(64) if (word >> b) & 1]
+        cpus = [c for c in cpus if c < os.cpu_count()]
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return len(cpus)
+    except Exception:  # no NVML / no affinity info: leave the scheduler alone
+        return None
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -496,9 +521,14 @@ def main():
     # ---- e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        # pinned host buffers on the GPU's own NUMA node (first touch under a
+        # temporary CPU binding; the scheduler's full set is restored at once)
+        all_cpus = os.sched_getaffinity(0)
+        numa_cpus = bind_host_to_gpu(local)
         host_ring = [t.cpu().pin_memory() for t in grads_ring[:1] + grads_ring[2:3]]
         host_ring = [host_ring[0], host_ring[0], host_ring[1], host_ring[1]]
         row = torch.empty(32, dtype=torch.uint8, pin_memory=True)
+        os.sched_setaffinity(0, all_cpus)
         gbufs[:] = [g, torch.empty_like(g)]
         st = make_step(0.3)
         run(st, max(3, args.warmup), host_ring=host_ring, host_row=row)
@@ -511,6 +541,7 @@ def main():
                "ms_per_step": e["ms"] / args.steps,
                "h2d_gbs_per_rank": 4 * P * args.steps / (e["ms"] * 1e-3) / 1e9,
                "serial_value": world * args.steps / (e_serial["ms"] / 1e3),
+               "host_cpus_bound": numa_cpus,
                "note": ("per step and rank: H2D of the fp32 gradient from pinned host memory, the "
                         "SelSync step (public blocking API), D2H of the decision row (bytes summed over "
                         "ranks); the gradient of step i+1 is copied on a side stream into a second "
