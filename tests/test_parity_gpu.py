@@ -301,3 +301,47 @@ def test_tensor_list_step_matches_flat_step():
     ra, rb = a.signal.read_trace()[:16], b.signal.read_trace()[:16]
     np.testing.assert_allclose(ra["grad_norm_sq"], rb["grad_norm_sq"], rtol=1e-12)
     assert 0 < sum(a.decision_log) < 16
+
+
+_PDL_SCRIPT = r"""
+import hashlib, sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2307_07950_b200 import SelSyncConfig
+from paper_2307_07950_b200.step import SelSyncStep
+dev = torch.device("cuda:0")
+gen = torch.Generator(device=dev).manual_seed(5)
+h = hashlib.sha256()
+for P in (1_002, 1_000_003):
+    w = (torch.rand(P, generator=gen, device=dev) - 0.5) * 0.1
+    grads = [torch.randn(P, generator=gen, device=dev) * s for s in (1.0, 1.0, 1.5, 1.5, 0.7)]
+    st = SelSyncStep(w, grads[0], SelSyncConfig(delta=0.2, warmup=2, smoothing=0.5, momentum=0.9,
+                                                weight_decay=4e-4))
+    for k in range(40):  # back to back: consecutive launches overlap under PDL
+        st.grads = grads[k % 5]
+        st.step_async(0.05)
+    st.synchronize()
+    for t in (st.params, st.momentum, st.signal.trace[: 32 * 40]):
+        h.update(t.cpu().numpy().tobytes())
+    h.update(bytes(st.decisions()))
+print(h.hexdigest())
+"""
+
+
+def test_programmatic_dependent_launch_changes_no_bit():
+    """Back-to-back steps launched with programmatic stream serialization
+    (the default) and without it (SS_PDL=0) give bit-identical parameters,
+    momentum, trace rows and decisions: no kernel touches memory before
+    griddepcontrol.wait returns."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    out = {}
+    for pdl in ("1", "0"):
+        p = subprocess.run([sys.executable, "-c", _PDL_SCRIPT, root], capture_output=True, text=True, timeout=300,
+                           env={**os.environ, "SS_PDL": pdl})
+        assert p.returncode == 0, p.stderr[-2000:]
+        out[pdl] = p.stdout.strip().splitlines()[-1]
+    assert out["1"] == out["0"]
