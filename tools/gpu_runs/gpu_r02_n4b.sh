@@ -3,7 +3,7 @@
 echo "HEAD $(cat .git_sha) + worktree"; nvidia-smi -L
 TR="python -m torch.distributed.run --nnodes=1 --master-addr=127.0.0.1 --master-port=29523"
 timeout 1500 python -m pytest tests/test_colocated_gpu.py tests/test_parity_gpu.py -x -q -m gpu -p no:cacheprovider > gpurun_out/b_colo.log 2>&1; echo colo rc=$?; tail -2 gpurun_out/b_colo.log
-bash tools/gpu_r02_nvls_ab.sh > gpurun_out/b_nvls_ab.txt 2>&1; echo nvls rc=$?
+bash tools/gpu_runs/gpu_r02_nvls_ab.sh > gpurun_out/b_nvls_ab.txt 2>&1; echo nvls rc=$?
 for n in 2 4; do
   for m in up up-noearly; do
     $TR --nproc-per-node $n tools/overlap_timeline.py 100000000 16384 $m 2>&1 | grep -v "OMP_NUM\|^\*\*\*\|^$" > gpurun_out/b_tl_n${n}_$m.txt; echo tl $n $m rc=$?
