@@ -149,7 +149,11 @@ def test_ticket_schedule_completes_and_orders_means(N, known, sync):
     G = 24
     for seed in range(6):
         T = random.Random(seed).choice([1, N - 1 if N > 1 else 1, 37, 101])
-        for lag in (G // (N + 1) + 2, 1, 0):
+        base = G // (N + 1) + 2
+        # the kernel's per-pass lags (nf_body): the known pass x3/4 over P2P,
+        # the pass after the ||g||^2 sweep x3/2, and the base; plus the extremes
+        scaled = (base - 2) * 3 // 4 + 2 if known else (base - 2) * 3 // 2 + 2
+        for lag in sorted({base, scaled, 1, 0}):
             simulate(N, G, T, lag, known, sync, seed)
 
 
