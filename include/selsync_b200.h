@@ -13,7 +13,14 @@
  *     the last failure on the calling thread is ss_last_error();
  *   - "dev" arguments are device pointers (HBM), "host" arguments live in host
  *     memory; device kernels are asynchronous on the given stream;
- *   - a workspace (ss_workspace_bytes) is owned by one stream at a time.
+ *   - a workspace (ss_workspace_bytes) is owned by one stream at a time;
+ *   - the norm, update and step kernels are launched with programmatic stream
+ *     serialization (programmatic dependent launch): their blocks may be
+ *     placed while the previous kernel in the stream drains, and each waits
+ *     (griddepcontrol.wait) for that kernel to complete before it touches
+ *     memory, so stream order is unchanged for every caller. They also
+ *     trigger their own dependents at entry. SS_PDL=0 in the environment
+ *     launches them without the attribute.
  *
  * Build: nvcc -gencode arch=compute_100a,code=sm_100a (see __graft_entry__.py).
  */
